@@ -1,0 +1,330 @@
+"""bench.py -- fused MHA fwd+bwd throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+
+A *step* is one pass of the hot path over the workload: mha_forward (O, lse)
+followed by mha_backward (dQ, dK, dV) through the C ABI of
+paper_2502_12784_b200/libvattn_b200.so.  Default workload = BASELINE configs[2]
+("C3"): causal, batch 4, heads 16, seq 8192, head_dim 128, bf16 -- the config
+that carries north_star's target (1 GPU, seq >= 4k, d = 128).
+
+Multi-GPU (torchrun, one process per GPU): every rank owns its own (batch,
+head) slab of a global batch of N x the per-GPU config -- the path is
+partitioned by (batch, head) with no collective on the data path ("weak").
+Timing: W warm-up steps, then K steps between barrier + synchronize, CUDA
+events on the launching stream, max over ranks.  Inputs (>= 4 x 128 MiB for
+C3) exceed the 126 MB L2, so no explicit flush.
+
+Reported: value = aggregate algorithmic TFLOPS (14 B H N^2 d c over all ranks /
+max-rank time; c = 1/2 causal), e2e = the same metric through the public API
+with host (pinned) buffers and the H2D/D2H copies inside the timed region,
+roofline = the fused backward main kernel (dominant) against the measured bf16
+tensor peak, cpu_baseline = the reference's CPU path (oracle/_ref) on a
+bounded sample.  `--impl reference` times the reference CPU path itself.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MHA fwd+bwd TFLOPS and % of B200 tensor peak at 1/2/4/8 GPUs vs CPU ref"
+
+CONFIGS = {
+    # name: (B, H, N, d, causal, dtype, description)
+    "c3": (4, 16, 8192, 128, True, "bf16", "BASELINE configs[2]: causal MHA fwd+bwd, d=128, B=4, H=16, N=8192, bf16"),
+    "c2_4k": (4, 32, 4096, 64, False, "fp16", "BASELINE configs[1] point: 16k tokens, hidden 2048, d=64, N=4096"),
+    "c2_16k": (1, 32, 16384, 64, False, "fp16", "BASELINE configs[1] point: 16k tokens, hidden 2048, d=64, N=16384"),
+    "c4": (8, 16, 1024, 64, True, "fp16", "BASELINE configs[3] per layer: GPT-2-medium attention, causal"),
+    "c5": (1, 64, 32768, 128, True, "bf16", "BASELINE configs[4] on one GPU: causal seq 32k, d=128, H=64"),
+}
+
+
+def flops(B, H, N, d, causal):
+    c = 0.5 if causal else 1.0
+    return 4.0 * B * H * N * N * d * c, 10.0 * B * H * N * N * d * c
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j.get("bf16_tflops"), j.get("bf16_tflops_sustained"), "measured"
+    return 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference_sample(d, causal, threads, n_cpu=1024):
+    """Reference CPU path (oracle/_ref: forward_fused FP32-ACC + backward_fused)
+    on `threads` (b,h) units of [1,1,n_cpu,d].  Returns (TFLOPS, seconds, sample text, kind)."""
+    from oracle import pyoracle as po
+    units = threads
+    f, b = flops(1, 1, n_cpu, d, causal)
+    if po.ref_available():
+        secs = po.ref_bench_units(n_cpu, d, causal, units, threads)
+        kind = "reference"
+    else:  # oracle port: restated FP32-ACC forward + binary64 gradients, single thread
+        import numpy as np
+        shape = (1, 1, n_cpu, d)
+        q, k, v, do = (po.normal16(1, s, shape) for s in (1, 2, 3, 4))
+        units, threads = 1, 1
+        t0 = time.perf_counter()
+        po.forward_fused_fp32acc(q, k, v, causal)
+        po.attention_grad_ref(po.widen(q), po.widen(k), po.widen(v), po.widen(do), causal)
+        secs = time.perf_counter() - t0
+        kind = "port"
+    if secs <= 0:
+        raise RuntimeError("reference CPU run failed")
+    tflops = units * (f + b) / secs / 1e12
+    sample = (f"{units} (b,h) units of [1,1,{n_cpu},{d}] {'causal' if causal else 'non-causal'} fp16, "
+              f"forward_fused FP32-ACC + backward_fused on {threads} host threads, {secs:.2f} s; "
+              f"algorithmic GFLOP/s is N-independent for the emulated tile loops")
+    return tflops, secs, sample, kind, threads
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    B, H, N, d, causal, dt, desc = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    vals = []
+    for _ in range(args.warmup):
+        cpu_reference_sample(d, causal, threads, n_cpu=256)
+    info = None
+    for _ in range(args.steps):
+        info = cpu_reference_sample(d, causal, threads)
+        vals.append(info[0])
+    val = statistics.median(vals)
+    tfl, secs, sample, kind, cores = info
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16 storage, f32 math (reference software model)",
+        "data": "synthetic (vattn::normal_tensor_f16 streams)",
+        "config": {"workload": desc, "cpu_sample": sample},
+        "cpu_baseline": {"value": val, "unit": "TFLOPS", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": val, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2502_12784_b200 as vb
+
+    B, H, N, d, causal, dt, desc = CONFIGS[args.config]
+    dtype = torch.bfloat16 if dt == "bf16" else torch.float16
+    dev = torch.device("cuda", local)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)  # each rank: its own (batch, head) slab of the global batch
+    shape = (B, H, N, d)
+    q, k, v, do = (torch.randn(shape, generator=gen, device=dev, dtype=torch.float32).to(dtype) for _ in range(4))
+    o = torch.empty_like(q)
+    lse = torch.empty((B, H, N), device=dev, dtype=torch.float32)
+    dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+    ws = torch.empty(vb.workspace_bytes(B, H, N, d, causal, dtype), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        vb.mha_forward(q, k, v, causal, out=o, lse=lse)
+        vb.mha_backward(q, k, v, o, do, lse, causal, dq=dq, dk=dk, dv=dv, workspace=ws)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- timed
+    vb.lib.vattn_profile_enable(1)
+    launches_per_step = 4  # fwd + (preprocess, fused bwd, dq split-reduce)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(stop)
+    import ctypes as C
+    f_ms, f_n, b_ms, b_n = C.c_double(), C.c_int(), C.c_double(), C.c_int()
+    vb.lib.vattn_profile_read(C.byref(f_ms), C.byref(f_n), C.byref(b_ms), C.byref(b_n))
+    vb.lib.vattn_profile_enable(0)
+    t = torch.tensor([ms, f_ms.value, b_ms.value], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, fwd_ms_tot, bwd_ms_tot = t.tolist()
+    ms_step = ms_max / args.steps
+    f_fwd, f_bwd = flops(B, H, N, d, causal)
+    value = world * (f_fwd + f_bwd) / (ms_step * 1e-3) / 1e12
+
+    # ------------------------------------------------------------------ e2e
+    # Public API with host buffers: pinned H2D of Q, K, V, dO; D2H of O, lse, dQ, dK, dV.
+    hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, do))
+    ho, hdq, hdk, hdv = (torch.empty(shape, dtype=dtype).pin_memory() for _ in range(4))
+    hlse = torch.empty((B, H, N), dtype=torch.float32).pin_memory()
+    h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo))
+    d2h = sum(x.numel() * x.element_size() for x in (ho, hlse, hdq, hdk, hdv))
+
+    def e2e_step():
+        q.copy_(hq, non_blocking=True)
+        k.copy_(hk, non_blocking=True)
+        v.copy_(hv, non_blocking=True)
+        do.copy_(hdo, non_blocking=True)
+        step()
+        ho.copy_(o, non_blocking=True)
+        hlse.copy_(lse, non_blocking=True)
+        hdq.copy_(dq, non_blocking=True)
+        hdk.copy_(dk, non_blocking=True)
+        hdv.copy_(dv, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = te.item() / args.e2e_steps
+    e2e_val = world * (f_fwd + f_bwd) / (e2e_ms * 1e-3) / 1e12
+
+    if rank == 0:
+        peak_burst, peak_sust, peak_src = measured_peaks()
+        bwd_ms = bwd_ms_tot / max(b_n.value, 1)
+        fwd_ms = fwd_ms_tot / max(f_n.value, 1)
+        achieved = f_bwd / (bwd_ms * 1e-3) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(args.config, {}).get("bwd_main_dram_bytes")
+            except Exception:
+                traffic = None
+        clk = clocks.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dt, "data": "synthetic (torch.randn, per-rank seed)",
+            "config": {"workload": desc, "batch_per_gpu": B, "heads": H, "seq_len": N, "head_dim": d,
+                       "causal": causal, "global_batch": B * world, "parallelism": f"(batch,head) shards x{world}, no collective",
+                       "l2": "inputs (4 x %d MiB) exceed the 126 MB L2; no flush" % (q.numel() * 2 >> 20),
+                       "flop_model": "fwd 4BHN^2d*c + bwd 10BHN^2d*c, c=1/2 causal"},
+            "pct_of_peak": value / world / peak_sust,
+            "fwd_ms": fwd_ms, "bwd_main_ms": bwd_ms,
+            "fwd_tflops": f_fwd / (fwd_ms * 1e-3) / 1e12,
+            "roofline": {"kernel": "mha_bwd_sm100_kernel", "bound": "tensor", "achieved": achieved,
+                         "peak": peak_sust, "peak_kind": f"bf16_tflops_sustained ({peak_src})",
+                         "unit": "TFLOP/s", "frac": achieved / peak_sust, "frac_of_burst": achieved / peak_burst,
+                         "traffic": traffic},
+            "e2e": {"value": e2e_val, "unit": "TFLOPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk,
+        }
+        if not args.no_cpu_baseline:
+            try:
+                tfl, secs, sample, kind, cores = cpu_reference_sample(d, causal, os.cpu_count() or 1)
+                line["cpu_baseline"] = {"value": tfl, "unit": "TFLOPS", "cores": cores, "kind": kind, "sample": sample}
+            except Exception as e:  # reported baseline only
+                line["cpu_baseline"] = {"value": None, "unit": "TFLOPS", "cores": 0, "kind": "unavailable",
+                                        "sample": f"failed: {e}"}
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

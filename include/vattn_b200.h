@@ -1,0 +1,102 @@
+/*
+ * vattn_b200.h -- C ABI of the B200 (sm_100a) fused multi-head-attention
+ * training path.  This is the drop-in boundary for the reference's operator
+ * API (arxiv 2502.12784 "SparkAttention", reference tree /root/reference/proj):
+ *
+ *   mha_forward   replaces vattn::forward_fused
+ *                 (proj/include/vattn/attention.hpp:51-52, proj/src/attention_forward.cpp:191-227)
+ *   mha_backward  replaces vattn::backward_fused
+ *                 (proj/include/vattn/backward.hpp:56-59, proj/src/attention_backward.cpp:59-219)
+ *                 including compute_dpsum (backward.hpp:43, attention_backward.cpp:44-57)
+ *                 and the DqAccumulator master buffer (backward.hpp:16-40)
+ *   vattn_config  mirrors vattn::AttnConfig (proj/include/vattn/attention.hpp:11-26)
+ *
+ * Conventions
+ *   - Tensors are device pointers, caller owned, dense row-major [B, H, N, d]
+ *     (proj/include/vattn/tensor.hpp:45-50); lse is [B, H, N] binary32 in
+ *     natural-log units (attention.hpp:30, online_softmax.cpp:84).
+ *   - 16-bit element type is fp16 (VATTN_F16, the reference's Half) or bf16.
+ *   - Calls are stream ordered and asynchronous; `stream` is a cudaStream_t
+ *     (NULL = legacy default stream).  Safe to call concurrently from several
+ *     host threads on different streams.
+ *   - Every call returns a vattn_status; on failure vattn_last_error() returns a
+ *     thread-local message.  VATTN_EINVAL corresponds to the reference's
+ *     std::invalid_argument, VATTN_EDOMAIN to std::domain_error.
+ *   - head_dim must be 64 or 128 at this boundary (the C++ layer
+ *     include/vattn_b200/mha.hpp zero-pads other head dims); any seq_len >= 1.
+ *   - No CPU fallback: when the sm_100a kernels cannot run, calls fail with
+ *     VATTN_ECUDA / VATTN_EUNSUPPORTED.
+ *
+ * Divergence from the reference (documented): the backward takes O as an
+ * input (D = rowsum(dO o O) is computed from it) instead of re-running the
+ * forward internally (attention_backward.cpp:91-104); the C++ layer provides
+ * the reference's six-argument overload by calling mha_forward first.
+ */
+#ifndef VATTN_B200_H
+#define VATTN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VATTN_B200_ABI_VERSION 1
+
+typedef enum vattn_status {
+    VATTN_OK = 0,
+    VATTN_EINVAL = 1,       /* bad config / shape / pointer  (std::invalid_argument) */
+    VATTN_EDOMAIN = 2,      /* numerical domain error        (std::domain_error)     */
+    VATTN_EUNSUPPORTED = 3, /* valid for the reference, not implemented here         */
+    VATTN_ECUDA = 4         /* CUDA runtime / launch failure, or no sm_100 device     */
+} vattn_status;
+
+typedef enum vattn_dtype { VATTN_F16 = 0, VATTN_BF16 = 1 } vattn_dtype;
+
+typedef struct vattn_config {
+    int32_t batch;          /* B >= 1                                              */
+    int32_t heads;          /* H >= 1                                              */
+    int32_t seq_len;        /* N >= 1                                              */
+    int32_t head_dim;       /* d in {64, 128}                                      */
+    int32_t causal;         /* top-left causal mask: key j visible iff j <= i      */
+    float softmax_scale;    /* <= 0 selects 1/sqrt(head_dim) (AttnConfig::scale)   */
+    int32_t dtype;          /* vattn_dtype                                         */
+} vattn_config;
+
+/* O = softmax(Q K^T * scale [+ causal mask]) V ;  lse = logsumexp per query row. */
+int mha_forward(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o,
+                float* lse, void* stream);
+
+/* Bytes of device workspace mha_backward needs for `cfg` (0 on invalid cfg). */
+size_t mha_backward_workspace_bytes(const vattn_config* cfg);
+
+/* dQ, dK, dV of the forward above given dO, O and lse.  `workspace` must hold
+ * mha_backward_workspace_bytes(cfg) bytes (256-byte aligned); its contents on
+ * entry are irrelevant.  dQ is reduced deterministically (bit-reproducible). */
+int mha_backward(const vattn_config* cfg, const void* q, const void* k, const void* v,
+                 const void* o, const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Thread-local description of the last failure on this thread ("" if none). */
+const char* vattn_last_error(void);
+
+/* VATTN_B200_ABI_VERSION of the loaded library. */
+int vattn_abi_version(void);
+
+/* Number of kernels the last successful call on this thread launched. */
+int vattn_last_launch_count(void);
+
+/* Measurement hooks (bench / roofline only; off by default).  When enabled,
+ * every call records CUDA events on its stream around the fused forward kernel
+ * and the fused backward main kernel; vattn_profile_read synchronizes those
+ * events and returns the summed kernel milliseconds and launch counts since the
+ * last vattn_profile_enable(1). */
+void vattn_profile_enable(int on);
+int vattn_profile_read(double* fwd_ms, int* fwd_launches, double* bwd_main_ms, int* bwd_launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VATTN_B200_H */

@@ -1,0 +1,268 @@
+"""paper_2502_12784_b200 -- B200 (sm_100a) fused multi-head-attention training path.
+
+Python mirror of the reference's operator API (arxiv 2502.12784, reference tree
+/root/reference/proj) over the C ABI in ``include/vattn_b200.h``:
+
+=====================  ==============================================================
+this module            reference
+=====================  ==============================================================
+``AttnConfig``         ``vattn::AttnConfig`` (include/vattn/attention.hpp:11-26)
+``forward_fused``      ``vattn::forward_fused`` (attention.hpp:51-52) -> (out, lse)
+``backward_fused``     ``vattn::backward_fused`` (backward.hpp:56-59) -> (dq, dk, dv)
+``mha_forward``        C ABI ``mha_forward`` on device tensors
+``mha_backward``       C ABI ``mha_backward`` on device tensors (takes O)
+``compute_dpsum``      ``vattn::compute_dpsum`` (backward.hpp:43), via the backward
+``MHAFunction``        torch.autograd binding (the paper's PyTorch layer)
+=====================  ==============================================================
+
+Errors mirror the reference: ``ValueError`` where it throws std::invalid_argument,
+``ArithmeticError`` for std::domain_error, ``NotImplementedError`` for
+unsupported-here, ``RuntimeError`` for CUDA failures.  There is no CPU fallback:
+the shared library is required, and importing this module fails loudly without it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+__all__ = [
+    "AttnConfig", "forward_fused", "backward_fused", "mha_forward", "mha_backward",
+    "workspace_bytes", "MHAFunction", "attention", "LIB_PATH", "lib",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvattn_b200.so")
+
+VATTN_OK, VATTN_EINVAL, VATTN_EDOMAIN, VATTN_EUNSUPPORTED, VATTN_ECUDA = range(5)
+VATTN_F16, VATTN_BF16 = 0, 1
+
+
+class _Cfg(C.Structure):
+    _fields_ = [
+        ("batch", C.c_int32), ("heads", C.c_int32), ("seq_len", C.c_int32), ("head_dim", C.c_int32),
+        ("causal", C.c_int32), ("softmax_scale", C.c_float), ("dtype", C.c_int32),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for this path)")
+    lib = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    lib.mha_forward.argtypes = [C.POINTER(_Cfg), vp, vp, vp, vp, vp, vp]
+    lib.mha_forward.restype = C.c_int
+    lib.mha_backward_workspace_bytes.argtypes = [C.POINTER(_Cfg)]
+    lib.mha_backward_workspace_bytes.restype = C.c_size_t
+    lib.mha_backward.argtypes = [C.POINTER(_Cfg)] + [vp] * 10 + [C.c_size_t, vp]
+    lib.mha_backward.restype = C.c_int
+    lib.vattn_last_error.restype = C.c_char_p
+    lib.vattn_abi_version.restype = C.c_int
+    lib.vattn_last_launch_count.restype = C.c_int
+    return lib
+
+
+lib = _load()
+
+
+def _raise(rc: int, where: str):
+    msg = f"{where}: {lib.vattn_last_error().decode()}"
+    if rc == VATTN_EINVAL:
+        raise ValueError(msg)
+    if rc == VATTN_EDOMAIN:
+        raise ArithmeticError(msg)
+    if rc == VATTN_EUNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise RuntimeError(msg)
+
+
+@dataclass
+class AttnConfig:
+    """vattn::AttnConfig (attention.hpp:11-26).  Tile sizes are validated for
+    compatibility with the reference but the GPU tiles are fixed at 128."""
+    batch: int = 1
+    heads: int = 1
+    seq_len: int = 0
+    head_dim: int = 0
+    tile_rows: int = 64
+    tile_cols: int = 64
+    causal: bool = False
+    dropout_p: float = 0.0
+    seed: int = 0
+    softmax_scale: float = 0.0
+
+    def validate(self, strict_tiles: bool = True) -> None:
+        """AttnConfig::validate (attention_forward.cpp:31-40).  ``strict_tiles=False``
+        drops the reference's N % tile requirement, which the GPU path does not need."""
+        def req(ok, msg):
+            if not ok:
+                raise ValueError(msg)
+        req(self.batch >= 1 and self.heads >= 1, "AttnConfig: batch and heads must be positive")
+        req(self.seq_len > 0 and self.head_dim > 0, "AttnConfig: seq_len and head_dim must be positive")
+        req(self.tile_rows > 0 and self.tile_rows % 8 == 0, "AttnConfig: tile_rows must be a positive multiple of 8")
+        req(self.tile_cols > 0 and self.tile_cols % 8 == 0, "AttnConfig: tile_cols must be a positive multiple of 8")
+        req(self.head_dim % 4 == 0, "AttnConfig: head_dim must be a multiple of 4")
+        if strict_tiles:
+            req(self.seq_len % self.tile_rows == 0, "AttnConfig: seq_len must be a multiple of tile_rows")
+            req(self.seq_len % self.tile_cols == 0, "AttnConfig: seq_len must be a multiple of tile_cols")
+        req(0.0 <= self.dropout_p < 1.0, "AttnConfig: dropout_p must be in [0, 1)")
+
+    def scale(self) -> float:
+        """AttnConfig::scale (attention_forward.cpp:42-45), binary32."""
+        if self.softmax_scale > 0.0:
+            return float(self.softmax_scale)
+        return float(torch.tensor(1.0, dtype=torch.float32) / torch.sqrt(torch.tensor(float(self.head_dim))))
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float16:
+        return VATTN_F16
+    if t.dtype == torch.bfloat16:
+        return VATTN_BF16
+    raise ValueError(f"tensors must be float16 or bfloat16, got {t.dtype}")
+
+
+def _cfg(q: torch.Tensor, causal: bool, softmax_scale: float) -> _Cfg:
+    B, H, N, d = q.shape
+    return _Cfg(B, H, N, d, 1 if causal else 0, float(softmax_scale), _dtype_code(q))
+
+
+def _check(ts, shape, dtype, names):
+    for t, n in zip(ts, names):
+        if t.shape != shape:
+            raise ValueError(f"{n} shape {tuple(t.shape)} != {tuple(shape)}")
+        if t.dtype != dtype:
+            raise ValueError(f"{n} dtype {t.dtype} != {dtype}")
+        if not t.is_cuda:
+            raise ValueError(f"{n} must be a CUDA tensor (no CPU fallback)")
+        if not t.is_contiguous():
+            raise ValueError(f"{n} must be contiguous [B, H, N, d]")
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _native_dim(d: int) -> int:
+    if d <= 64:
+        return 64
+    if d <= 128:
+        return 128
+    raise NotImplementedError(f"head_dim {d} > 128 is not supported")
+
+
+def _pad(t: torch.Tensor, dn: int) -> torch.Tensor:
+    return t if t.shape[-1] == dn else torch.nn.functional.pad(t, (0, dn - t.shape[-1])).contiguous()
+
+
+def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=None, lse=None):
+    """C ABI ``mha_forward`` on CUDA tensors [B, H, N, d] (d in {64, 128}).
+    Returns (out, lse) with lse [B, H, N] fp32 natural-log."""
+    _check((q, k, v), q.shape, q.dtype, ("q", "k", "v"))
+    B, H, N, d = q.shape
+    out = torch.empty_like(q) if out is None else out
+    lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
+    cfg = _cfg(q, causal, softmax_scale)
+    rc = lib.mha_forward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                         lse.data_ptr(), _stream())
+    if rc:
+        _raise(rc, "mha_forward")
+    return out, lse
+
+
+def workspace_bytes(B, H, N, d, causal=False, dtype=torch.float16) -> int:
+    cfg = _Cfg(B, H, N, d, 1 if causal else 0, 0.0, VATTN_BF16 if dtype == torch.bfloat16 else VATTN_F16)
+    return int(lib.mha_backward_workspace_bytes(C.byref(cfg)))
+
+
+def mha_backward(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: float = 0.0,
+                 dq=None, dk=None, dv=None, workspace=None):
+    """C ABI ``mha_backward`` on CUDA tensors.  Returns (dq, dk, dv)."""
+    _check((q, k, v, o, dout), q.shape, q.dtype, ("q", "k", "v", "o", "dout"))
+    B, H, N, d = q.shape
+    if lse.shape != (B, H, N) or lse.dtype != torch.float32 or not lse.is_contiguous():
+        raise ValueError("lse must be a contiguous float32 [B, H, N] tensor")
+    cfg = _cfg(q, causal, softmax_scale)
+    need = int(lib.mha_backward_workspace_bytes(C.byref(cfg)))
+    if need == 0:
+        rc = lib.mha_backward(C.byref(cfg), *([None] * 10), 0, None)
+        _raise(rc if rc else VATTN_EINVAL, "mha_backward")
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(q) if dk is None else dk
+    dv = torch.empty_like(q) if dv is None else dv
+    rc = lib.mha_backward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                          dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                          workspace.data_ptr(), workspace.numel(), _stream())
+    if rc:
+        _raise(rc, "mha_backward")
+    return dq, dk, dv
+
+
+# ----------------------------------------- reference-shaped operator API --
+
+def _prep(cfg: AttnConfig, *ts):
+    cfg.validate(strict_tiles=False)
+    if cfg.dropout_p > 0.0:
+        raise NotImplementedError("dropout is not on this path (BASELINE north_star runs p = 0)")
+    shape = (cfg.batch, cfg.heads, cfg.seq_len, cfg.head_dim)
+    for t in ts:
+        if tuple(t.shape) != shape:
+            raise ValueError(f"tensor shape {tuple(t.shape)} does not match config {shape}")
+    dn = _native_dim(cfg.head_dim)
+    return [_pad(t.contiguous(), dn) for t in ts], dn
+
+
+def forward_fused(q, k, v, cfg: AttnConfig):
+    """vattn::forward_fused on CUDA tensors: returns (out, lse).  head_dim other
+    than 64/128 is zero-padded (exact: padded columns add 0 to every dot product)."""
+    (qp, kp, vp), dn = _prep(cfg, q, k, v)
+    out, lse = mha_forward(qp, kp, vp, cfg.causal, cfg.scale())
+    return out[..., : cfg.head_dim].contiguous(), lse
+
+
+def backward_fused(q, k, v, d_out, lse, cfg: AttnConfig, out=None):
+    """vattn::backward_fused on CUDA tensors: returns (dq, dk, dv).  Like the
+    reference (attention_backward.cpp:91-104) it recomputes O with the forward
+    when ``out`` is not given."""
+    (qp, kp, vp, dop), dn = _prep(cfg, q, k, v, d_out)
+    if out is None:
+        op, _ = mha_forward(qp, kp, vp, cfg.causal, cfg.scale())
+    else:
+        op = _pad(out.contiguous(), dn)
+    dq, dk, dv = mha_backward(qp, kp, vp, op, dop, lse.contiguous(), cfg.causal, cfg.scale())
+    d = cfg.head_dim
+    return dq[..., :d].contiguous(), dk[..., :d].contiguous(), dv[..., :d].contiguous()
+
+
+class MHAFunction(torch.autograd.Function):
+    """torch.autograd binding: forward = mha_forward, backward = mha_backward."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, causal=False, softmax_scale=0.0):
+        d = q.shape[-1]
+        dn = _native_dim(d)
+        qp, kp, vp = (_pad(x.contiguous(), dn) for x in (q, k, v))
+        scale = softmax_scale if softmax_scale > 0 else 1.0 / math.sqrt(d)
+        o, lse = mha_forward(qp, kp, vp, causal, scale)
+        ctx.save_for_backward(qp, kp, vp, o, lse)
+        ctx.causal, ctx.scale, ctx.d = causal, scale, d
+        return o[..., :d] if dn != d else o
+
+    @staticmethod
+    def backward(ctx, do):
+        qp, kp, vp, o, lse = ctx.saved_tensors
+        dop = _pad(do.contiguous(), qp.shape[-1])
+        dq, dk, dv = mha_backward(qp, kp, vp, o, dop, lse, ctx.causal, ctx.scale)
+        d = ctx.d
+        return dq[..., :d], dk[..., :d], dv[..., :d], None, None
+
+
+def attention(q, k, v, causal: bool = False, softmax_scale: float = 0.0):
+    """Differentiable fused attention on [B, H, N, d] fp16/bf16 CUDA tensors."""
+    return MHAFunction.apply(q, k, v, causal, softmax_scale)

@@ -1,0 +1,370 @@
+// capi.cu -- the C ABI (include/vattn_b200.h) over the sm_100a kernels.
+//
+// Host-side responsibilities: validate the config the way AttnConfig::validate
+// does (reference proj/src/attention_forward.cpp:31-40, plus the B200 limits),
+// build TMA descriptors for the [B*H, N, d] tensors, size/carve the backward
+// workspace, and launch.  There is no CPU or library fallback anywhere.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/vattn_b200.h"
+#include "mha_bwd_sm100.cuh"
+#include "mha_fwd_sm100.cuh"
+
+using namespace vattn_sm100;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+// ---- measurement hooks (vattn_profile_*): event pairs around the hot kernels
+struct ProfPair {
+    cudaEvent_t a, b;
+    int kind;  // 0 fwd, 1 bwd main
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfPair> g_prof;
+
+struct ProfScope {
+    cudaStream_t s;
+    int kind;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(cudaStream_t s_, int kind_) : s(s_), kind(kind_) {
+        bool on;
+        {
+            std::lock_guard<std::mutex> l(g_prof_mu);
+            on = g_prof_on;
+        }
+        if (!on) return;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        cudaEventRecord(b, s);
+        std::lock_guard<std::mutex> l(g_prof_mu);
+        g_prof.push_back({a, b, kind});
+    }
+};
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(ptr);
+    });
+    return fn;
+}
+
+// [B*H, N, d] 16-bit tensor, 128 rows x 64 columns per box, 128-byte swizzle.
+bool make_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(N),
+                                static_cast<cuuint64_t>(BH)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2,
+                                   static_cast<cuuint64_t>(D) * 2 * static_cast<cuuint64_t>(N)};
+    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r =
+        enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+            const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// sm_100 check, cached per device.
+int check_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(VATTN_ECUDA, "no CUDA device");
+    static int cached[64];
+    static std::once_flag flags[64];
+    if (dev < 0 || dev >= 64) return fail(VATTN_ECUDA, "device index out of range");
+    std::call_once(flags[dev], [dev] {
+        int major = 0, minor = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        cached[dev] = major * 10 + minor;
+    });
+    if (cached[dev] != 100)
+        return fail(VATTN_ECUDA, "vattn_b200 kernels are built for sm_100a (B200); device is sm_" +
+                                     std::to_string(cached[dev]));
+    return VATTN_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int validate(const vattn_config* c) {
+    if (!c) return fail(VATTN_EINVAL, "vattn_config: null");
+    if (c->batch < 1 || c->heads < 1)
+        return fail(VATTN_EINVAL, "AttnConfig: batch and heads must be positive");
+    if (c->seq_len < 1 || c->head_dim < 1)
+        return fail(VATTN_EINVAL, "AttnConfig: seq_len and head_dim must be positive");
+    if (c->dtype != VATTN_F16 && c->dtype != VATTN_BF16)
+        return fail(VATTN_EINVAL, "vattn_config: dtype must be VATTN_F16 or VATTN_BF16");
+    if (c->causal != 0 && c->causal != 1) return fail(VATTN_EINVAL, "vattn_config: causal must be 0/1");
+    if (!std::isfinite(c->softmax_scale)) return fail(VATTN_EINVAL, "vattn_config: softmax_scale not finite");
+    if (c->head_dim != 64 && c->head_dim != 128)
+        return fail(VATTN_EUNSUPPORTED, "head_dim must be 64 or 128 at the C ABI (pad in the caller)");
+    const long long bh = static_cast<long long>(c->batch) * c->heads;
+    if (bh > 65535) return fail(VATTN_EUNSUPPORTED, "batch * heads must be <= 65535");
+    if (bh * c->seq_len > (1ll << 31) - 1)
+        return fail(VATTN_EUNSUPPORTED, "batch * heads * seq_len must fit in int32");
+    return VATTN_OK;
+}
+
+float eff_scale(const vattn_config* c) {
+    // AttnConfig::scale(), proj/src/attention_forward.cpp:42-45
+    return c->softmax_scale > 0.0f ? c->softmax_scale
+                                   : 1.0f / std::sqrt(static_cast<float>(c->head_dim));
+}
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int kD, bool kBF16>
+int launch_forward(const vattn_config* c, const void* q, const void* k, const void* v, void* o,
+                   float* lse, cudaStream_t stream) {
+    const int BH = c->batch * c->heads, N = c->seq_len;
+    CUtensorMap mq, mk, mv, mo;
+    if (!make_map(&mq, q, BH, N, kD, kBF16) || !make_map(&mk, k, BH, N, kD, kBF16) ||
+        !make_map(&mv, v, BH, N, kD, kBF16) || !make_map(&mo, o, BH, N, kD, kBF16))
+        return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled failed");
+    auto kern = mha_fwd_sm100_kernel<kD, kBF16>;
+    constexpr int smem = FwdCfg<kD>::kSmemBytes;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    });
+    if (attr_err != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(attr_err));
+    FwdParams p;
+    p.lse = lse;
+    p.N = N;
+    p.n_kv = (N + 127) / 128;
+    p.causal = c->causal;
+    p.scale_log2 = eff_scale(c) * kLog2e;
+    dim3 grid((N + 255) / 256, BH);
+    {
+        ProfScope prof(stream, 0);
+        kern<<<grid, FwdCfg<kD>::kThreads, smem, stream>>>(mq, mk, mv, mo, p);
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("mha_fwd launch: ") + cudaGetErrorString(e));
+    g_launches = 1;
+    return VATTN_OK;
+}
+
+struct BwdLayout {
+    size_t dq_acc, lse2, dsum, sems, ticket, total;
+    int n_q, Npad, n_groups;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+BwdLayout bwd_layout(const vattn_config* c) {
+    BwdLayout L{};
+    const size_t BH = static_cast<size_t>(c->batch) * c->heads;
+    const size_t N = c->seq_len, D = c->head_dim;
+    L.n_q = static_cast<int>((N + 127) / 128);
+    L.Npad = L.n_q * 128;
+    L.n_groups = (L.n_q + kBwdGroup - 1) / kBwdGroup;
+    size_t off = 0;
+    L.dq_acc = off;
+    off = align256(off + static_cast<size_t>(L.n_groups) * BH * N * D * 4);
+    L.lse2 = off;
+    off = align256(off + BH * L.Npad * 4);
+    L.dsum = off;
+    off = align256(off + BH * L.Npad * 4);
+    L.sems = off;
+    off = align256(off + static_cast<size_t>(L.n_groups) * BH * L.n_q * 4);
+    L.ticket = off;
+    off = align256(off + 4);
+    L.total = off;
+    return L;
+}
+
+template <int kD, bool kBF16>
+int launch_backward(const vattn_config* c, const void* q, const void* k, const void* v,
+                    const void* o, const void* dout, const float* lse, void* dq, void* dk,
+                    void* dv, void* ws, cudaStream_t stream) {
+    const int BH = c->batch * c->heads, N = c->seq_len;
+    const BwdLayout L = bwd_layout(c);
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    float* dq_acc = reinterpret_cast<float*>(w + L.dq_acc);
+    float* lse2 = reinterpret_cast<float*>(w + L.lse2);
+    float* dsum = reinterpret_cast<float*>(w + L.dsum);
+    int* sems = reinterpret_cast<int*>(w + L.sems);
+    int* ticket = reinterpret_cast<int*>(w + L.ticket);
+    const int n_sems = L.n_groups * BH * L.n_q;
+
+    CUtensorMap mq, mk, mv, mdo;
+    if (!make_map(&mq, q, BH, N, kD, kBF16) || !make_map(&mk, k, BH, N, kD, kBF16) ||
+        !make_map(&mv, v, BH, N, kD, kBF16) || !make_map(&mdo, dout, BH, N, kD, kBF16))
+        return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled failed");
+
+    // 1) D, lse2, zeroed semaphores / ticket
+    {
+        const long long rows = static_cast<long long>(BH) * L.Npad;
+        long long blocks = (rows + 7) / 8;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        mha_bwd_preprocess_kernel<kD, kBF16><<<static_cast<int>(blocks), 256, 0, stream>>>(
+            o, dout, lse, lse2, dsum, sems, n_sems, ticket, N, L.Npad, BH);
+    }
+    // 2) fused backward
+    {
+        auto kern = mha_bwd_sm100_kernel<kD, kBF16>;
+        constexpr int smem = BwdCfg<kD>::kSmemBytes;
+        static std::once_flag once;
+        static cudaError_t attr_err = cudaSuccess;
+        std::call_once(once, [&] {
+            attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        });
+        if (attr_err != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(attr_err));
+        BwdParams p;
+        p.lse2 = lse2;
+        p.dsum = dsum;
+        p.dq_acc = dq_acc;
+        p.sems = sems;
+        p.ticket = ticket;
+        p.dk = dk;
+        p.dv = dv;
+        p.N = N;
+        p.Npad = L.Npad;
+        p.BH = BH;
+        p.n_q = L.n_q;
+        p.causal = c->causal;
+        p.scale = eff_scale(c);
+        p.scale_log2 = p.scale * kLog2e;
+        ProfScope prof(stream, 1);
+        kern<<<BH * L.n_q, 512, smem, stream>>>(mq, mk, mv, mdo, p);
+    }
+    // 3) split reduction of the dQ partials, one rounding
+    {
+        const long long n4 = static_cast<long long>(BH) * N * kD / 4;
+        long long blocks = (n4 + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        mha_dq_convert_kernel<kD, kBF16><<<static_cast<int>(blocks), 256, 0, stream>>>(
+            dq_acc, dq, N, BH, L.n_groups, c->causal, eff_scale(c));
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("mha_bwd launch: ") + cudaGetErrorString(e));
+    g_launches = 3;
+    return VATTN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vattn_abi_version(void) { return VATTN_B200_ABI_VERSION; }
+
+const char* vattn_last_error(void) { return g_err.c_str(); }
+
+int vattn_last_launch_count(void) { return g_launches; }
+
+void vattn_profile_enable(int on) {
+    std::lock_guard<std::mutex> l(g_prof_mu);
+    for (auto& e : g_prof) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    g_prof.clear();
+    g_prof_on = on != 0;
+}
+
+int vattn_profile_read(double* fwd_ms, int* fwd_launches, double* bwd_main_ms, int* bwd_launches) {
+    std::lock_guard<std::mutex> l(g_prof_mu);
+    double f = 0, b = 0;
+    int nf = 0, nb = 0;
+    for (auto& e : g_prof) {
+        if (cudaEventSynchronize(e.b) != cudaSuccess) return fail(VATTN_ECUDA, "profile event sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e.a, e.b);
+        if (e.kind == 0) {
+            f += ms;
+            ++nf;
+        } else {
+            b += ms;
+            ++nb;
+        }
+    }
+    if (fwd_ms) *fwd_ms = f;
+    if (fwd_launches) *fwd_launches = nf;
+    if (bwd_main_ms) *bwd_main_ms = b;
+    if (bwd_launches) *bwd_launches = nb;
+    return VATTN_OK;
+}
+
+int mha_forward(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o,
+                float* lse, void* stream) {
+    g_launches = 0;
+    int rc = validate(cfg);
+    if (rc) return rc;
+    if (!q || !k || !v || !o || !lse) return fail(VATTN_EINVAL, "mha_forward: null tensor pointer");
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+        return fail(VATTN_EINVAL, "mha_forward: tensors must be 16-byte aligned");
+    if ((rc = check_device())) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool bf = cfg->dtype == VATTN_BF16;
+    if (cfg->head_dim == 64)
+        return bf ? launch_forward<64, true>(cfg, q, k, v, o, lse, s)
+                  : launch_forward<64, false>(cfg, q, k, v, o, lse, s);
+    return bf ? launch_forward<128, true>(cfg, q, k, v, o, lse, s)
+              : launch_forward<128, false>(cfg, q, k, v, o, lse, s);
+}
+
+size_t mha_backward_workspace_bytes(const vattn_config* cfg) {
+    if (validate(cfg)) return 0;
+    return bwd_layout(cfg).total;
+}
+
+int mha_backward(const vattn_config* cfg, const void* q, const void* k, const void* v,
+                 const void* o, const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                 void* workspace, size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    int rc = validate(cfg);
+    if (rc) return rc;
+    if (!q || !k || !v || !o || !dout || !lse || !dq || !dk || !dv || !workspace)
+        return fail(VATTN_EINVAL, "mha_backward: null pointer");
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(dout) ||
+        !aligned16(dq) || !aligned16(dk) || !aligned16(dv))
+        return fail(VATTN_EINVAL, "mha_backward: tensors must be 16-byte aligned");
+    if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0)
+        return fail(VATTN_EINVAL, "mha_backward: workspace must be 256-byte aligned");
+    if (workspace_bytes < bwd_layout(cfg).total)
+        return fail(VATTN_EINVAL, "mha_backward: workspace too small (see mha_backward_workspace_bytes)");
+    if ((rc = check_device())) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool bf = cfg->dtype == VATTN_BF16;
+    if (cfg->head_dim == 64)
+        return bf ? launch_backward<64, true>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, s)
+                  : launch_backward<64, false>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, s);
+    return bf ? launch_backward<128, true>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, s)
+              : launch_backward<128, false>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,328 @@
+// mha_fwd_sm100.cuh -- fused multi-head-attention forward for sm_100a.
+//
+// Replaces vattn::forward_fused (reference: proj/src/attention_forward.cpp:191-227,
+// per-unit body run_forward_unit :110-187).  Same contract: S = Q K^T * scale,
+// top-left causal mask (key j visible iff j <= i, :128 and :140-144), online
+// softmax (proj/src/online_softmax.cpp:21-87), P rounded to 16 bit exactly
+// once before P V (:163-167), O = acc / l rounded once (:179), and
+// lse = m + ln(l) in natural-log units (online_softmax.cpp:84).
+//
+// One CTA = one (batch*head, 256-query block) = two 128-row Q tiles that share
+// every K/V tile staged in shared memory:
+//   warp 0      TMA producer: Q0, Q1 once; K_j, V_j through a STAGES-deep ring
+//   warp 1      MMA issuer (one thread): S_t = Q_t K_j^T (SS), O_t += P_t V_j (TS:
+//               P read from tensor memory, V from shared memory, MN-major)
+//   warp 2      TMEM allocator
+//   warps 4-7   softmax for tile 0 (thread = query row = TMEM lane)
+//   warps 8-11  softmax for tile 1
+// Tensor memory (512 columns): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D, 256+2D).
+// P_t (16-bit, two per column) overwrites the first 64 columns of S_t.
+// The MMA issue order S0(j+1) right after PV0(j), S1(j+1) right after PV1(j)
+// keeps the tensor pipe busy while the other tile's softmax runs.
+// O is rescaled lazily: only when a row maximum grows by more than 2^8.
+#pragma once
+
+#include "sm100_ptx.cuh"
+
+namespace vattn_sm100 {
+
+struct FwdParams {
+    float* lse;          // [BH, N] natural-log logsumexp
+    int N;               // sequence length
+    int n_kv;            // ceil(N / 128)
+    int causal;
+    float scale_log2;    // softmax_scale * log2(e)
+};
+
+template <int kD>
+struct FwdCfg {
+    static constexpr int kTileBytes = kD * 128 * 2;     // one 128-row 16-bit tile
+    static constexpr int kBoxes = kD / 64;              // 64-column TMA boxes per tile
+    static constexpr int kStages = kD == 128 ? 4 : 8;   // K/V ring depth
+    static constexpr int kSmemQ = 0;                    // Q0, Q1
+    static constexpr int kSmemKV = 2 * kTileBytes;
+    static constexpr int kSmemBar = kSmemKV + kStages * kTileBytes;
+    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 + 2;
+    static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
+    static constexpr int kThreads = 384;
+    static constexpr uint32_t kTmemO = 256;
+};
+
+template <int kD, bool kBF16>
+__global__ void __launch_bounds__(384, 1)
+    mha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
+                         const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v,
+                         const __grid_constant__ CUtensorMap tm_o, const FwdParams p) {
+    using Cfg = FwdCfg<kD>;
+    constexpr int S = Cfg::kStages;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sQ = smem + Cfg::kSmemQ;
+    uint8_t* sKV = smem + Cfg::kSmemKV;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kSmemBar);
+    uint64_t* q_full = bars;
+    uint64_t* kv_full = bars + 1;
+    uint64_t* kv_empty = kv_full + S;
+    uint64_t* s_full = kv_empty + S;
+    uint64_t* p_full = s_full + 2;
+    uint64_t* o_done = p_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
+
+    const int warp = warp_id();
+    const int lane = lane_id();
+    const int bh = blockIdx.y;
+    const int nqb = gridDim.x;
+    const int qblk = p.causal ? (nqb - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
+    const int q0 = qblk * 256;
+    const int N = p.N;
+
+    int nk[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int r0 = q0 + 128 * t;
+        nk[t] = r0 >= N ? 0 : (p.causal ? (r0 / 128 + 1) : p.n_kv);
+    }
+    const int nkmax = nk[0] > nk[1] ? nk[0] : nk[1];
+
+    if (threadIdx.x == 0) {
+        if ((smem_u32(smem) & 1023u) != 0) __trap();
+        mbar_init(q_full, 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(kv_full + s, 1);
+            mbar_init(kv_empty + s, 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(s_full + t, 1);
+            mbar_init(p_full + t, 128);
+            mbar_init(o_done + t, 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            tma_prefetch_desc(&tm_q);
+            tma_prefetch_desc(&tm_k);
+            tma_prefetch_desc(&tm_v);
+            tma_prefetch_desc(&tm_o);
+            const int nvalid = (nk[0] > 0) + (nk[1] > 0);
+            mbar_arrive_expect_tx(q_full, nvalid * Cfg::kTileBytes);
+            for (int t = 0; t < 2; ++t) {
+                if (nk[t] == 0) continue;
+                for (int b = 0; b < Cfg::kBoxes; ++b)
+                    tma_load_3d(sQ + t * Cfg::kTileBytes + b * 16384, &tm_q, q_full, b * 64,
+                                q0 + 128 * t, bh);
+            }
+            for (int j = 0; j < nkmax; ++j) {
+#pragma unroll
+                for (int w = 0; w < 2; ++w) {
+                    const int pos = 2 * j + w;
+                    const int slot = pos % S;
+                    const uint32_t ph = (pos / S) & 1;
+                    mbar_wait(kv_empty + slot, ph ^ 1);
+                    mbar_arrive_expect_tx(kv_full + slot, Cfg::kTileBytes);
+                    uint8_t* dst = sKV + slot * Cfg::kTileBytes;
+                    const CUtensorMap* map = w == 0 ? &tm_k : &tm_v;
+                    for (int b = 0; b < Cfg::kBoxes; ++b)
+                        tma_load_3d(dst + b * 16384, map, kv_full + slot, b * 64, j * 128, bh);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // -------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc_s = umma_idesc_f16(128, 128, kBF16, 0, 0);
+            constexpr uint32_t idesc_o = umma_idesc_f16(128, kD, kBF16, 0, 1);
+            const uint32_t sQa = smem_u32(sQ);
+            const uint32_t sKVa = smem_u32(sKV);
+            auto issue_s = [&](int t, int j) {
+                const uint32_t kbase = sKVa + ((2 * j) % S) * Cfg::kTileBytes;
+                const uint32_t qbase = sQa + t * Cfg::kTileBytes;
+#pragma unroll
+                for (int kk = 0; kk < kD / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    mma_ss(tmem + 128 * t, umma_desc_sw128(qbase + off, 16, 1024),
+                           umma_desc_sw128(kbase + off, 16, 1024), idesc_s, kk > 0);
+                }
+                mma_commit(s_full + t);
+            };
+            auto issue_pv = [&](int t, int j) {
+                const uint32_t vbase = sKVa + ((2 * j + 1) % S) * Cfg::kTileBytes;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    mma_ts(tmem + Cfg::kTmemO + kD * t, tmem + 128 * t + kk * 8,
+                           umma_desc_sw128(vbase + kk * 2048, 16384, 1024), idesc_o,
+                           (j > 0 || kk > 0) ? 1u : 0u);
+                }
+                mma_commit(o_done + t);
+            };
+            auto wait_kv = [&](int pos) {
+                mbar_wait(kv_full + (pos % S), (pos / S) & 1);
+                tc_fence_after();
+            };
+            mbar_wait(q_full, 0);
+            tc_fence_after();
+            if (nkmax > 0) {
+                wait_kv(0);
+                for (int t = 0; t < 2; ++t)
+                    if (nk[t] > 0) issue_s(t, 0);
+                mma_commit(kv_empty + 0);
+            }
+            for (int j = 0; j < nkmax; ++j) {
+                wait_kv(2 * j + 1);
+                bool k_next = false;
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    if (j < nk[t]) {
+                        mbar_wait(p_full + t, j & 1);
+                        tc_fence_after();
+                        issue_pv(t, j);
+                        if (j + 1 < nk[t]) {
+                            if (!k_next) {
+                                wait_kv(2 * j + 2);
+                                k_next = true;
+                            }
+                            issue_s(t, j + 1);
+                        }
+                    }
+                }
+                mma_commit(kv_empty + (2 * j + 1) % S);
+                if (k_next) mma_commit(kv_empty + (2 * j + 2) % S);
+            }
+        }
+    } else if (warp >= 4) {
+        // ----------------------------------------------------------- softmax
+        const int t = (warp - 4) >> 2;           // Q tile of this warpgroup
+        const int r = ((warp & 3) << 5) + lane;  // row within tile == TMEM lane
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint32_t tS = tmem + lane_base + 128 * t;
+        const uint32_t tO = tmem + lane_base + Cfg::kTmemO + kD * t;
+        const int row = q0 + 128 * t + r;
+        const float sc = p.scale_log2;
+        float m_run = -INFINITY;  // running max, log2 units (already scaled)
+        float l_run = 0.0f;
+        const int ntile = nk[t];
+        for (int j = 0; j < ntile; ++j) {
+            mbar_wait(s_full + t, j & 1);
+            tc_fence_after();
+            float s[128];
+            {
+                uint32_t u0[32], u1[32], u2[32], u3[32];
+                tmem_ld32(tS + 0, u0);
+                tmem_ld32(tS + 32, u1);
+                tmem_ld32(tS + 64, u2);
+                tmem_ld32(tS + 96, u3);
+                tmem_wait_ld();
+#pragma unroll
+                for (int x = 0; x < 32; ++x) {
+                    s[x] = __uint_as_float(u0[x]);
+                    s[32 + x] = __uint_as_float(u1[x]);
+                    s[64 + x] = __uint_as_float(u2[x]);
+                    s[96 + x] = __uint_as_float(u3[x]);
+                }
+            }
+            // masking: causal diagonal tile (keys > row) or keys beyond N
+            int lim = 127;
+            if (p.causal && j == ntile - 1) lim = r;  // diagonal: j*128 == tile row base
+            if (!p.causal && j == p.n_kv - 1) lim = min(lim, N - j * 128 - 1);
+            if (lim < 127) {
+#pragma unroll
+                for (int c = 0; c < 128; ++c)
+                    if (c > lim) s[c] = -INFINITY;
+            }
+            float mx = s[0];
+#pragma unroll
+            for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+            const float m_tile = mx * sc;
+            if (j == 0) {
+                m_run = m_tile;
+            } else if (__any_sync(0xffffffffu, m_tile > m_run + 8.0f)) {
+                // Lazy rescale (warp-uniform: tcgen05.ld/st are .sync.aligned).  The
+                // previous P V must have landed before O is touched.  Rows whose max
+                // did not grow enough keep their stale max (factor 1).
+                float f = 1.0f;
+                if (m_tile > m_run) {
+                    f = ex2(m_run - m_tile);
+                    m_run = m_tile;
+                }
+                l_run *= f;
+                mbar_wait(o_done + t, (j - 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < kD / 32; ++c) {
+                    uint32_t u[32];
+                    tmem_ld32(tO + 32 * c, u);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) u[x] = __float_as_uint(__uint_as_float(u[x]) * f);
+                    tmem_st32(tO + 32 * c, u);
+                }
+            }
+            const float m_use = m_run == -INFINITY ? 0.0f : m_run;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t pk[32];
+#pragma unroll
+                for (int x = 0; x < 32; ++x) {
+                    const float p0 = ex2(fmaf(s[64 * c + 2 * x], sc, -m_use));
+                    const float p1 = ex2(fmaf(s[64 * c + 2 * x + 1], sc, -m_use));
+                    l_run += p0 + p1;
+                    pk[x] = pack2<kBF16>(p0, p1);
+                }
+                tmem_st32(tS + 32 * c, pk);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(p_full + t);
+        }
+        if (ntile > 0) {
+            // ------------------------------------------------------ epilogue
+            mbar_wait(o_done + t, (ntile - 1) & 1);
+            tc_fence_after();
+            const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+            if (row < N) {
+                const float m_use = m_run == -INFINITY ? 0.0f : m_run;
+                p.lse[static_cast<size_t>(bh) * N + row] = (m_use + lg2(l_run)) * 0.69314718055994530942f;
+            }
+            uint8_t* sO = sQ + t * Cfg::kTileBytes;  // Q_t is dead once the last S_t landed
+#pragma unroll
+            for (int c = 0; c < kD / 32; ++c) {
+                uint32_t u[32];
+                tmem_ld32(tO + 32 * c, u);
+                tmem_wait_ld();
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    uint4 v;
+                    v.x = pack2<kBF16>(__uint_as_float(u[8 * x + 0]) * inv_l, __uint_as_float(u[8 * x + 1]) * inv_l);
+                    v.y = pack2<kBF16>(__uint_as_float(u[8 * x + 2]) * inv_l, __uint_as_float(u[8 * x + 3]) * inv_l);
+                    v.z = pack2<kBF16>(__uint_as_float(u[8 * x + 4]) * inv_l, __uint_as_float(u[8 * x + 5]) * inv_l);
+                    v.w = pack2<kBF16>(__uint_as_float(u[8 * x + 6]) * inv_l, __uint_as_float(u[8 * x + 7]) * inv_l);
+                    const int col = 32 * c + 8 * x;  // first of 8 columns
+                    st_swz128(sO + (col >> 6) * 16384, r, (col & 63) >> 3, v);
+                }
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1 + t, 128);
+            if (warp == 4 + 4 * t && lane == 0) {
+                for (int b = 0; b < Cfg::kBoxes; ++b)
+                    tma_store_3d(&tm_o, sO + b * 16384, b * 64, q0 + 128 * t, bh);
+                bulk_commit();
+                bulk_wait_read0();
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+}  // namespace vattn_sm100
