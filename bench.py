@@ -153,11 +153,12 @@ def run_reference(args):
     B, H, N, d, causal, dt, desc = CONFIGS[args.config]
     threads = os.cpu_count() or 1
     vals = []
+    # Each step is a bounded sample (~0.5 s on 16 cores) so --steps 50 ends in well under a minute.
     for _ in range(args.warmup):
-        cpu_reference_sample(d, causal, threads, n_cpu=256)
+        cpu_reference_sample(d, causal, threads, n_cpu=128)
     info = None
     for _ in range(args.steps):
-        info = cpu_reference_sample(d, causal, threads)
+        info = cpu_reference_sample(d, causal, threads, n_cpu=256)
         vals.append(info[0])
     val = statistics.median(vals)
     tfl, secs, sample, kind, cores = info
@@ -220,7 +221,7 @@ def main():
 
     # ---------------------------------------------------------------- timed
     vb.lib.vattn_profile_enable(1)
-    launches_per_step = 4  # fwd + (preprocess, fused bwd, dq split-reduce)
+    launches_per_step = 4  # fwd + (preprocess, dK/dV kernel, dQ kernel)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -235,13 +236,16 @@ def main():
         dist.barrier()
     ms = start.elapsed_time(stop)
     import ctypes as C
-    f_ms, f_n, b_ms, b_n = C.c_double(), C.c_int(), C.c_double(), C.c_int()
-    vb.lib.vattn_profile_read(C.byref(f_ms), C.byref(f_n), C.byref(b_ms), C.byref(b_n))
+    kern_ms = []
+    for kind in (0, 1, 2):  # VATTN_KERNEL_FWD, _BWD_DKDV, _BWD_DQ
+        t_ms, n_l = C.c_double(), C.c_int()
+        vb.lib.vattn_profile_read(kind, C.byref(t_ms), C.byref(n_l))
+        kern_ms.append(t_ms.value / max(n_l.value, 1))
     vb.lib.vattn_profile_enable(0)
-    t = torch.tensor([ms, f_ms.value, b_ms.value], device=dev, dtype=torch.float64)
+    t = torch.tensor([ms] + kern_ms, device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, fwd_ms_tot, bwd_ms_tot = t.tolist()
+    ms_max, fwd_ms, dkdv_ms, dq_ms = t.tolist()
     ms_step = ms_max / args.steps
     f_fwd, f_bwd = flops(B, H, N, d, causal)
     value = world * (f_fwd + f_bwd) / (ms_step * 1e-3) / 1e12
@@ -284,14 +288,15 @@ def main():
 
     if rank == 0:
         peak_burst, peak_sust, peak_src = measured_peaks()
-        bwd_ms = bwd_ms_tot / max(b_n.value, 1)
-        fwd_ms = fwd_ms_tot / max(f_n.value, 1)
-        achieved = f_bwd / (bwd_ms * 1e-3) / 1e12
+        # dominant kernel: the key-major dK/dV kernel (4 of the 5 algorithmic
+        # backward GEMMs: S^T, dP^T, dV, dK = 8 B H N^2 d c flops per launch)
+        f_dkdv = 0.8 * f_bwd
+        achieved = f_dkdv / (dkdv_ms * 1e-3) / 1e12
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(args.config, {}).get("bwd_main_dram_bytes")
+                traffic = json.load(open(tp)).get(args.config, {}).get("bwd_dkdv_dram_bytes")
             except Exception:
                 traffic = None
         clk = clocks.summary()
@@ -304,9 +309,12 @@ def main():
                        "l2": "inputs (4 x %d MiB) exceed the 126 MB L2; no flush" % (q.numel() * 2 >> 20),
                        "flop_model": "fwd 4BHN^2d*c + bwd 10BHN^2d*c, c=1/2 causal"},
             "pct_of_peak": value / world / peak_sust,
-            "fwd_ms": fwd_ms, "bwd_main_ms": bwd_ms,
+            "kernels_ms": {"fwd": fwd_ms, "bwd_dkdv": dkdv_ms, "bwd_dq": dq_ms,
+                           "bwd_other(preprocess)": ms_step - fwd_ms - dkdv_ms - dq_ms},
             "fwd_tflops": f_fwd / (fwd_ms * 1e-3) / 1e12,
-            "roofline": {"kernel": "mha_bwd_sm100_kernel", "bound": "tensor", "achieved": achieved,
+            "bwd_tflops": f_bwd / ((ms_step - fwd_ms) * 1e-3) / 1e12,
+            "dq_kernel_tflops_executed": 0.6 * f_bwd / (dq_ms * 1e-3) / 1e12,
+            "roofline": {"kernel": "mha_bwd_dkdv_kernel", "bound": "tensor", "achieved": achieved,
                          "peak": peak_sust, "peak_kind": f"bf16_tflops_sustained ({peak_src})",
                          "unit": "TFLOP/s", "frac": achieved / peak_sust, "frac_of_burst": achieved / peak_burst,
                          "traffic": traffic},

@@ -73,7 +73,8 @@ size_t mha_backward_workspace_bytes(const vattn_config* cfg);
 
 /* dQ, dK, dV of the forward above given dO, O and lse.  `workspace` must hold
  * mha_backward_workspace_bytes(cfg) bytes (256-byte aligned); its contents on
- * entry are irrelevant.  dQ is reduced deterministically (bit-reproducible). */
+ * entry are irrelevant.  All three gradients are bit-reproducible run to run
+ * (no atomics; dQ is accumulated over key tiles in a fixed order). */
 int mha_backward(const vattn_config* cfg, const void* q, const void* k, const void* v,
                  const void* o, const void* dout, const float* lse, void* dq, void* dk, void* dv,
                  void* workspace, size_t workspace_bytes, void* stream);
@@ -88,12 +89,15 @@ int vattn_abi_version(void);
 int vattn_last_launch_count(void);
 
 /* Measurement hooks (bench / roofline only; off by default).  When enabled,
- * every call records CUDA events on its stream around the fused forward kernel
- * and the fused backward main kernel; vattn_profile_read synchronizes those
- * events and returns the summed kernel milliseconds and launch counts since the
- * last vattn_profile_enable(1). */
+ * every call records CUDA events on its stream around the hot kernels;
+ * vattn_profile_read(kind) synchronizes those events and returns the summed
+ * kernel milliseconds and launch count of one kernel kind since the last
+ * vattn_profile_enable(1).  Kinds: */
+#define VATTN_KERNEL_FWD 0     /* fused forward                      */
+#define VATTN_KERNEL_BWD_DKDV 1 /* backward, key-major dK / dV kernel */
+#define VATTN_KERNEL_BWD_DQ 2   /* backward, query-major dQ kernel    */
 void vattn_profile_enable(int on);
-int vattn_profile_read(double* fwd_ms, int* fwd_launches, double* bwd_main_ms, int* bwd_launches);
+int vattn_profile_read(int kind, double* ms_total, int* launches);
 
 #ifdef __cplusplus
 }

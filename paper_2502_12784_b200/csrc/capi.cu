@@ -179,8 +179,8 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
 }
 
 struct BwdLayout {
-    size_t dq_acc, lse2, dsum, sems, ticket, total;
-    int n_q, Npad, n_groups;
+    size_t lse2, dsum, total;
+    int n_q, Npad;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -188,23 +188,22 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 BwdLayout bwd_layout(const vattn_config* c) {
     BwdLayout L{};
     const size_t BH = static_cast<size_t>(c->batch) * c->heads;
-    const size_t N = c->seq_len, D = c->head_dim;
-    L.n_q = static_cast<int>((N + 127) / 128);
+    L.n_q = (c->seq_len + 127) / 128;
     L.Npad = L.n_q * 128;
-    L.n_groups = (L.n_q + kBwdGroup - 1) / kBwdGroup;
-    size_t off = 0;
-    L.dq_acc = off;
-    off = align256(off + static_cast<size_t>(L.n_groups) * BH * N * D * 4);
-    L.lse2 = off;
-    off = align256(off + BH * L.Npad * 4);
-    L.dsum = off;
-    off = align256(off + BH * L.Npad * 4);
-    L.sems = off;
-    off = align256(off + static_cast<size_t>(L.n_groups) * BH * L.n_q * 4);
-    L.ticket = off;
-    off = align256(off + 4);
-    L.total = off;
+    L.lse2 = 0;
+    L.dsum = align256(BH * L.Npad * 4);
+    L.total = L.dsum + align256(BH * L.Npad * 4);
     return L;
+}
+
+// One cudaFuncSetAttribute per kernel instantiation (keyed on the kernel itself:
+// different instantiations share a function-pointer type).
+template <auto kKernel>
+cudaError_t set_smem_once(int bytes) {
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    std::call_once(once, [&] { err = cudaFuncSetAttribute(kKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
+    return err;
 }
 
 template <int kD, bool kBF16>
@@ -214,61 +213,49 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     const int BH = c->batch * c->heads, N = c->seq_len;
     const BwdLayout L = bwd_layout(c);
     uint8_t* w = static_cast<uint8_t*>(ws);
-    float* dq_acc = reinterpret_cast<float*>(w + L.dq_acc);
     float* lse2 = reinterpret_cast<float*>(w + L.lse2);
     float* dsum = reinterpret_cast<float*>(w + L.dsum);
-    int* sems = reinterpret_cast<int*>(w + L.sems);
-    int* ticket = reinterpret_cast<int*>(w + L.ticket);
-    const int n_sems = L.n_groups * BH * L.n_q;
 
-    CUtensorMap mq, mk, mv, mdo;
+    CUtensorMap mq, mk, mv, mdo, mdq;
     if (!make_map(&mq, q, BH, N, kD, kBF16) || !make_map(&mk, k, BH, N, kD, kBF16) ||
-        !make_map(&mv, v, BH, N, kD, kBF16) || !make_map(&mdo, dout, BH, N, kD, kBF16))
+        !make_map(&mv, v, BH, N, kD, kBF16) || !make_map(&mdo, dout, BH, N, kD, kBF16) ||
+        !make_map(&mdq, dq, BH, N, kD, kBF16))
         return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled failed");
 
-    // 1) D, lse2, zeroed semaphores / ticket
+    // 1) D = rowsum(dO o O), lse2 = lse * log2(e)
     {
         const long long rows = static_cast<long long>(BH) * L.Npad;
         long long blocks = (rows + 7) / 8;
         if (blocks > 148 * 16) blocks = 148 * 16;
         mha_bwd_preprocess_kernel<kD, kBF16><<<static_cast<int>(blocks), 256, 0, stream>>>(
-            o, dout, lse, lse2, dsum, sems, n_sems, ticket, N, L.Npad, BH);
+            o, dout, lse, lse2, dsum, N, L.Npad, BH);
     }
-    // 2) fused backward
+    BwdParams p;
+    p.lse2 = lse2;
+    p.dsum = dsum;
+    p.N = N;
+    p.Npad = L.Npad;
+    p.n_q = L.n_q;
+    p.causal = c->causal;
+    p.scale = eff_scale(c);
+    p.scale_log2 = p.scale * kLog2e;
+    // 2) dK, dV (key-major)
     {
-        auto kern = mha_bwd_sm100_kernel<kD, kBF16>;
-        constexpr int smem = BwdCfg<kD>::kSmemBytes;
-        static std::once_flag once;
-        static cudaError_t attr_err = cudaSuccess;
-        std::call_once(once, [&] {
-            attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        });
-        if (attr_err != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(attr_err));
-        BwdParams p;
-        p.lse2 = lse2;
-        p.dsum = dsum;
-        p.dq_acc = dq_acc;
-        p.sems = sems;
-        p.ticket = ticket;
-        p.dk = dk;
-        p.dv = dv;
-        p.N = N;
-        p.Npad = L.Npad;
-        p.BH = BH;
-        p.n_q = L.n_q;
-        p.causal = c->causal;
-        p.scale = eff_scale(c);
-        p.scale_log2 = p.scale * kLog2e;
+        auto kern = mha_bwd_dkdv_kernel<kD, kBF16>;
+        constexpr int smem = DkdvCfg<kD>::kSmemBytes;
+        const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16>>(smem);
+        if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
-        kern<<<BH * L.n_q, 512, smem, stream>>>(mq, mk, mv, mdo, p);
+        kern<<<dim3(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, dk, dv, p);
     }
-    // 3) split reduction of the dQ partials, one rounding
+    // 3) dQ (query-major, fixed-order accumulation in TMEM)
     {
-        const long long n4 = static_cast<long long>(BH) * N * kD / 4;
-        long long blocks = (n4 + 255) / 256;
-        if (blocks > 148 * 8) blocks = 148 * 8;
-        mha_dq_convert_kernel<kD, kBF16><<<static_cast<int>(blocks), 256, 0, stream>>>(
-            dq_acc, dq, N, BH, L.n_groups, c->causal, eff_scale(c));
+        auto kern = mha_bwd_dq_kernel<kD, kBF16>;
+        constexpr int smem = DqCfg<kD>::kSmemBytes;
+        const cudaError_t ae = set_smem_once<mha_bwd_dq_kernel<kD, kBF16>>(smem);
+        if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
+        ProfScope prof(stream, 2);
+        kern<<<dim3(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, mdq, p);
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("mha_bwd launch: ") + cudaGetErrorString(e));
@@ -279,6 +266,22 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
 }  // namespace
 
 extern "C" {
+
+#ifdef VATTN_TRACE
+// Debug-only: select the backward work item to trace / read its timeline.
+int vattn_trace_select(int item) {
+    cudaMemcpyToSymbol(g_vattn_trace_block, &item, sizeof(int));
+    long long z[4096] = {0};
+    cudaMemcpyToSymbol(g_vattn_trace, z, sizeof(z));
+    return 0;
+}
+int vattn_trace_read(long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_vattn_trace, sizeof(long long) * (n < 4096 ? n : 4096)) ==
+                   cudaSuccess
+               ? 0
+               : 1;
+}
+#endif
 
 int vattn_abi_version(void) { return VATTN_B200_ABI_VERSION; }
 
@@ -296,26 +299,20 @@ void vattn_profile_enable(int on) {
     g_prof_on = on != 0;
 }
 
-int vattn_profile_read(double* fwd_ms, int* fwd_launches, double* bwd_main_ms, int* bwd_launches) {
+int vattn_profile_read(int kind, double* ms_total, int* launches) {
     std::lock_guard<std::mutex> l(g_prof_mu);
-    double f = 0, b = 0;
-    int nf = 0, nb = 0;
+    double t = 0;
+    int n = 0;
     for (auto& e : g_prof) {
+        if (e.kind != kind) continue;
         if (cudaEventSynchronize(e.b) != cudaSuccess) return fail(VATTN_ECUDA, "profile event sync");
         float ms = 0;
         cudaEventElapsedTime(&ms, e.a, e.b);
-        if (e.kind == 0) {
-            f += ms;
-            ++nf;
-        } else {
-            b += ms;
-            ++nb;
-        }
+        t += ms;
+        ++n;
     }
-    if (fwd_ms) *fwd_ms = f;
-    if (fwd_launches) *fwd_launches = nf;
-    if (bwd_main_ms) *bwd_main_ms = b;
-    if (bwd_launches) *bwd_launches = nb;
+    if (ms_total) *ms_total = t;
+    if (launches) *launches = n;
     return VATTN_OK;
 }
 

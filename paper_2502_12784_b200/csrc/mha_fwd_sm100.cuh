@@ -42,7 +42,7 @@ struct FwdCfg {
     static constexpr int kSmemQ = 0;                    // Q0, Q1
     static constexpr int kSmemKV = 2 * kTileBytes;
     static constexpr int kSmemBar = kSmemKV + kStages * kTileBytes;
-    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 + 2;
+    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 4 + 2;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr int kThreads = 384;
     static constexpr uint32_t kTmemO = 256;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* kv_empty = kv_full + S;
     uint64_t* s_full = kv_empty + S;
     uint64_t* p_full = s_full + 2;
-    uint64_t* o_done = p_full + 2;
+    uint64_t* o_done = p_full + 4;  // p_full: [tile][half]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
     const int warp = warp_id();
@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(s_full + t, 1);
-            mbar_init(p_full + t, 128);
+            mbar_init(p_full + 2 * t, 128);
+            mbar_init(p_full + 2 * t + 1, 128);
             mbar_init(o_done + t, 1);
         }
         fence_barrier_init();
@@ -103,6 +104,9 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // registers: producer/MMA warpgroup 88, softmax warpgroups 208 (384 x 168 budget);
+    // each role lowers/raises its own budget inside its branch.
+    if (warp < 4) regs_dec<88>();
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
@@ -155,10 +159,16 @@ __global__ void __launch_bounds__(384, 1)
             auto issue_pv = [&](int t, int j) {
                 const uint32_t vbase = sKVa + ((2 * j + 1) % S) * Cfg::kTileBytes;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    mma_ts(tmem + Cfg::kTmemO + kD * t, tmem + 128 * t + kk * 8,
-                           umma_desc_sw128(vbase + kk * 2048, 16384, 1024), idesc_o,
-                           (j > 0 || kk > 0) ? 1u : 0u);
+                for (int hf = 0; hf < 2; ++hf) {
+                    mbar_wait(p_full + 2 * t + hf, j & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; ++k4) {
+                        const int kk = 4 * hf + k4;
+                        mma_ts(tmem + Cfg::kTmemO + kD * t, tmem + 128 * t + kk * 8,
+                               umma_desc_sw128(vbase + kk * 2048, 16384, 1024), idesc_o,
+                               (j > 0 || kk > 0) ? 1u : 0u);
+                    }
                 }
                 mma_commit(o_done + t);
             };
@@ -180,8 +190,6 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
                     if (j < nk[t]) {
-                        mbar_wait(p_full + t, j & 1);
-                        tc_fence_after();
                         issue_pv(t, j);
                         if (j + 1 < nk[t]) {
                             if (!k_next) {
@@ -198,6 +206,7 @@ __global__ void __launch_bounds__(384, 1)
         }
     } else if (warp >= 4) {
         // ----------------------------------------------------------- softmax
+        regs_inc<208>();
         const int t = (warp - 4) >> 2;           // Q tile of this warpgroup
         const int r = ((warp & 3) << 5) + lane;  // row within tile == TMEM lane
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -212,21 +221,11 @@ __global__ void __launch_bounds__(384, 1)
             mbar_wait(s_full + t, j & 1);
             tc_fence_after();
             float s[128];
-            {
-                uint32_t u0[32], u1[32], u2[32], u3[32];
-                tmem_ld32(tS + 0, u0);
-                tmem_ld32(tS + 32, u1);
-                tmem_ld32(tS + 64, u2);
-                tmem_ld32(tS + 96, u3);
-                tmem_wait_ld();
-#pragma unroll
-                for (int x = 0; x < 32; ++x) {
-                    s[x] = __uint_as_float(u0[x]);
-                    s[32 + x] = __uint_as_float(u1[x]);
-                    s[64 + x] = __uint_as_float(u2[x]);
-                    s[96 + x] = __uint_as_float(u3[x]);
-                }
-            }
+            tmem_ld32f(tS + 0, s);
+            tmem_ld32f(tS + 32, s + 32);
+            tmem_ld32f(tS + 64, s + 64);
+            tmem_ld32f(tS + 96, s + 96);
+            tmem_wait_ld();
             // masking: causal diagonal tile (keys > row) or keys beyond N
             int lim = 127;
             if (p.causal && j == ntile - 1) lim = r;  // diagonal: j*128 == tile row base
@@ -265,6 +264,8 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
             const float m_use = m_run == -INFINITY ? 0.0f : m_run;
+            // P in two halves (keys [0,64) then [64,128)): the MMA warp starts the
+            // first half of P V while the second half is still being exponentiated.
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 uint32_t pk[32];
@@ -276,10 +277,10 @@ __global__ void __launch_bounds__(384, 1)
                     pk[x] = pack2<kBF16>(p0, p1);
                 }
                 tmem_st32(tS + 32 * c, pk);
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(p_full + 2 * t + c);
             }
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(p_full + t);
         }
         if (ntile > 0) {
             // ------------------------------------------------------ epilogue

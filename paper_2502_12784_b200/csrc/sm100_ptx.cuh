@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
+#include <cstdio>
 
 #define VATTN_DEV __device__ __forceinline__
 
@@ -21,6 +22,12 @@ VATTN_DEV uint32_t smem_u32(const void* p) {
 
 VATTN_DEV uint32_t warp_id() { return threadIdx.x >> 5; }
 VATTN_DEV uint32_t lane_id() { return threadIdx.x & 31; }
+
+// Per-warpgroup register budget hand-off (all 4 warps of the warpgroup execute it).
+template <uint32_t kRegs>
+VATTN_DEV void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs)); }
+template <uint32_t kRegs>
+VATTN_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs)); }
 
 // Named barrier over `nthreads` threads (id 0 is __syncthreads).
 VATTN_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
@@ -78,7 +85,11 @@ VATTN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint64_t t0 = globaltimer_ns();
     uint32_t n = 0;
     while (!mbar_try_wait(bar, parity)) {
-        if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) __trap();
+        if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) {
+            printf("vattn watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n",
+                   (int)(blockIdx.x + blockIdx.y * gridDim.x), (int)threadIdx.x, smem_u32(bar), parity);
+            __trap();
+        }
     }
 #else
     while (!mbar_try_wait(bar, parity)) {
@@ -198,6 +209,20 @@ VATTN_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         : "r"(taddr));
 }
 
+// Same as tmem_ld32 but straight into fp32 registers.
+VATTN_DEV void tmem_ld32f(uint32_t taddr, float* f) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=f"(f[0]), "=f"(f[1]), "=f"(f[2]), "=f"(f[3]), "=f"(f[4]), "=f"(f[5]), "=f"(f[6]),
+          "=f"(f[7]), "=f"(f[8]), "=f"(f[9]), "=f"(f[10]), "=f"(f[11]), "=f"(f[12]), "=f"(f[13]),
+          "=f"(f[14]), "=f"(f[15]), "=f"(f[16]), "=f"(f[17]), "=f"(f[18]), "=f"(f[19]),
+          "=f"(f[20]), "=f"(f[21]), "=f"(f[22]), "=f"(f[23]), "=f"(f[24]), "=f"(f[25]),
+          "=f"(f[26]), "=f"(f[27]), "=f"(f[28]), "=f"(f[29]), "=f"(f[30]), "=f"(f[31])
+        : "r"(taddr));
+}
+
 VATTN_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -263,6 +288,24 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t M, uint32_t N, ui
            | ((M >> 4) << 24);
 }
 
+// ------------------------------------------------------------ debug trace --
+// Build with -DVATTN_TRACE: kernels stamp clock64() of pipeline events of the
+// CTA selected by g_vattn_trace_block into g_vattn_trace (read back through
+// vattn_trace_read()).  Compiled out otherwise.
+#ifdef VATTN_TRACE
+__device__ long long g_vattn_trace[4096];
+__device__ int g_vattn_trace_block;
+#define VTRACE(slot)                                                                  \
+    do {                                                                             \
+        if (static_cast<int>(blockIdx.x + blockIdx.y * gridDim.x) == g_vattn_trace_block) \
+            g_vattn_trace[(slot)] = clock64();                                       \
+    } while (0)
+#else
+#define VTRACE(slot) \
+    do {             \
+    } while (0)
+#endif
+
 // ------------------------------------------------------------ conversions --
 
 template <bool kBF16>
@@ -315,6 +358,9 @@ VATTN_DEV int ld_acquire_gpu(const int* p) {
 VATTN_DEV void st_release_gpu(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+
+// Release-side fence for the dQ turn hand-off (lighter than __threadfence's fence.sc).
+VATTN_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 VATTN_DEV void red_add_v4(float* p, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
