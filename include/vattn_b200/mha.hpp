@@ -1,0 +1,235 @@
+// vattn_b200/mha.hpp -- C++ operator API of the B200 fused-MHA training path.
+//
+// Header-only layer over the C ABI (include/vattn_b200.h) that mirrors the
+// reference's operator surface (arxiv 2502.12784, /root/reference/proj):
+//
+//   vattn_b200::AttnConfig      <- vattn::AttnConfig     (include/vattn/attention.hpp:11-26)
+//   vattn_b200::ForwardOutput   <- vattn::ForwardOutput  (attention.hpp:28-33)
+//   vattn_b200::GradOutputs     <- vattn::GradOutputs    (include/vattn/backward.hpp:10-14)
+//   vattn_b200::forward_fused   <- vattn::forward_fused  (attention.hpp:51-52)
+//   vattn_b200::backward_fused  <- vattn::backward_fused (backward.hpp:56-59)
+//
+// Host tensors use the reference layout (dense row-major [B, H, N, d], binary16
+// bit patterns; lse [B, H, N] binary32).  Each call allocates device buffers,
+// copies in, runs the sm_100a kernels through the C ABI on `stream`, copies
+// out and synchronizes -- the drop-in for the reference's synchronous CPU
+// calls.  The *_device overloads take caller-owned device pointers and are
+// asynchronous (what benchmarks and training loops use).  Errors are thrown as
+// the reference throws them: std::invalid_argument for config/shape problems,
+// std::domain_error for numerical-domain problems, std::runtime_error for CUDA
+// failures (there is no CPU fallback).
+//
+// head_dim values other than 64/128 (any d <= 128 with d % 4 == 0, as the
+// reference allows) are zero-padded on the device: padded Q/K columns add 0 to
+// every dot product, padded V columns produce 0 output columns that are dropped.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../vattn_b200.h"
+
+namespace vattn_b200 {
+
+struct AttnConfig {
+    int batch = 1;
+    int heads = 1;
+    int seq_len = 0;
+    int head_dim = 0;
+    int tile_rows = 64;  // validated like the reference; the GPU tiles are fixed at 128
+    int tile_cols = 64;
+    bool causal = false;
+    float dropout_p = 0.0f;
+    uint64_t seed = 0;
+    float softmax_scale = 0.0f;  // <= 0 picks 1/sqrt(head_dim)
+    vattn_dtype dtype = VATTN_F16;
+
+    // AttnConfig::validate (proj/src/attention_forward.cpp:31-40), minus the
+    // N % tile requirement the GPU path does not need.
+    void validate() const {
+        auto req = [](bool ok, const char* m) {
+            if (!ok) throw std::invalid_argument(m);
+        };
+        req(batch >= 1 && heads >= 1, "AttnConfig: batch and heads must be positive");
+        req(seq_len > 0 && head_dim > 0, "AttnConfig: seq_len and head_dim must be positive");
+        req(tile_rows > 0 && tile_rows % 8 == 0, "AttnConfig: tile_rows must be a positive multiple of 8");
+        req(tile_cols > 0 && tile_cols % 8 == 0, "AttnConfig: tile_cols must be a positive multiple of 8");
+        req(head_dim % 4 == 0, "AttnConfig: head_dim must be a multiple of 4");
+        req(dropout_p >= 0.0f && dropout_p < 1.0f, "AttnConfig: dropout_p must be in [0, 1)");
+    }
+    // AttnConfig::scale (attention_forward.cpp:42-45)
+    float scale() const {
+        return softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt(static_cast<float>(head_dim));
+    }
+    size_t elems() const {
+        return static_cast<size_t>(batch) * heads * seq_len * head_dim;
+    }
+    size_t rows() const { return static_cast<size_t>(batch) * heads * seq_len; }
+};
+
+struct ForwardOutput {
+    std::vector<uint16_t> out;  // [B, H, N, d] 16-bit bit patterns
+    std::vector<float> lse;     // [B, H, N]
+};
+
+struct GradOutputs {
+    std::vector<uint16_t> dq, dk, dv;  // [B, H, N, d]
+};
+
+namespace detail {
+
+inline void check(int rc, const char* where) {
+    if (rc == VATTN_OK) return;
+    const std::string msg = std::string(where) + ": " + vattn_last_error();
+    if (rc == VATTN_EINVAL) throw std::invalid_argument(msg);
+    if (rc == VATTN_EDOMAIN) throw std::domain_error(msg);
+    if (rc == VATTN_EUNSUPPORTED) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+inline void cuda(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(size_t bytes) { cuda(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc"); }
+    ~DevBuf() { cudaFree(p); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+inline int native_dim(int d) {
+    if (d <= 64) return 64;
+    if (d <= 128) return 128;
+    throw std::invalid_argument("head_dim > 128 is not supported on the B200 path");
+}
+
+// host [rows, d] -> device [rows, dn] zero padded
+inline void upload_padded(void* dst, const uint16_t* src, size_t rows, int d, int dn, cudaStream_t s) {
+    if (d == dn) {
+        cuda(cudaMemcpyAsync(dst, src, rows * d * 2, cudaMemcpyHostToDevice, s), "H2D");
+        return;
+    }
+    cuda(cudaMemsetAsync(dst, 0, rows * dn * 2, s), "memset");
+    cuda(cudaMemcpy2DAsync(dst, dn * 2, src, d * 2, d * 2, rows, cudaMemcpyHostToDevice, s), "H2D 2D");
+}
+
+inline void download_padded(uint16_t* dst, const void* src, size_t rows, int d, int dn, cudaStream_t s) {
+    cuda(cudaMemcpy2DAsync(dst, d * 2, src, dn * 2, d * 2, rows, cudaMemcpyDeviceToHost, s), "D2H");
+}
+
+inline vattn_config to_c(const AttnConfig& c, int dn) {
+    vattn_config r;
+    r.batch = c.batch;
+    r.heads = c.heads;
+    r.seq_len = c.seq_len;
+    r.head_dim = dn;
+    r.causal = c.causal ? 1 : 0;
+    r.softmax_scale = c.scale();  // scale of the true head_dim, not the padded one
+    r.dtype = c.dtype;
+    return r;
+}
+
+}  // namespace detail
+
+// ---------------------------------------------------------- device overloads
+
+inline void forward_fused_device(const AttnConfig& cfg, const void* q, const void* k, const void* v,
+                                 void* out, float* lse, cudaStream_t stream = nullptr) {
+    cfg.validate();
+    if (cfg.head_dim != 64 && cfg.head_dim != 128)
+        throw std::invalid_argument("forward_fused_device: head_dim must be 64 or 128 (use the host overload to pad)");
+    if (cfg.dropout_p > 0.0f) throw std::invalid_argument("dropout is not on the B200 path");
+    const vattn_config c = detail::to_c(cfg, cfg.head_dim);
+    detail::check(mha_forward(&c, q, k, v, out, lse, stream), "mha_forward");
+}
+
+inline void backward_fused_device(const AttnConfig& cfg, const void* q, const void* k,
+                                  const void* v, const void* out, const void* d_out,
+                                  const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                                  size_t workspace_bytes, cudaStream_t stream = nullptr) {
+    cfg.validate();
+    if (cfg.head_dim != 64 && cfg.head_dim != 128)
+        throw std::invalid_argument("backward_fused_device: head_dim must be 64 or 128");
+    if (cfg.dropout_p > 0.0f) throw std::invalid_argument("dropout is not on the B200 path");
+    const vattn_config c = detail::to_c(cfg, cfg.head_dim);
+    detail::check(mha_backward(&c, q, k, v, out, d_out, lse, dq, dk, dv, workspace, workspace_bytes, stream),
+                  "mha_backward");
+}
+
+// ------------------------------------------------------------ host overloads
+
+// vattn::forward_fused: host [B,H,N,d] binary16 in, ForwardOutput out.
+inline ForwardOutput forward_fused(const std::vector<uint16_t>& q, const std::vector<uint16_t>& k,
+                                   const std::vector<uint16_t>& v, const AttnConfig& cfg) {
+    cfg.validate();
+    if (cfg.dropout_p > 0.0f) throw std::invalid_argument("dropout is not on the B200 path");
+    if (q.size() != cfg.elems() || k.size() != cfg.elems() || v.size() != cfg.elems())
+        throw std::invalid_argument("forward_fused: Q/K/V shape mismatch");
+    const int dn = detail::native_dim(cfg.head_dim);
+    const size_t rows = cfg.rows();
+    cudaStream_t s = nullptr;
+    detail::DevBuf dq(rows * dn * 2), dk(rows * dn * 2), dv(rows * dn * 2), dout(rows * dn * 2),
+        dlse(rows * 4);
+    detail::upload_padded(dq.p, q.data(), rows, cfg.head_dim, dn, s);
+    detail::upload_padded(dk.p, k.data(), rows, cfg.head_dim, dn, s);
+    detail::upload_padded(dv.p, v.data(), rows, cfg.head_dim, dn, s);
+    const vattn_config c = detail::to_c(cfg, dn);
+    detail::check(mha_forward(&c, dq.p, dk.p, dv.p, dout.p, static_cast<float*>(dlse.p), s), "mha_forward");
+    ForwardOutput r;
+    r.out.resize(cfg.elems());
+    r.lse.resize(rows);
+    detail::download_padded(r.out.data(), dout.p, rows, cfg.head_dim, dn, s);
+    detail::cuda(cudaMemcpyAsync(r.lse.data(), dlse.p, rows * 4, cudaMemcpyDeviceToHost, s), "D2H lse");
+    detail::cuda(cudaStreamSynchronize(s), "sync");
+    return r;
+}
+
+// vattn::backward_fused (6-argument form): the reference re-runs the forward to
+// obtain O (attention_backward.cpp:91-104); so does this overload.
+inline GradOutputs backward_fused(const std::vector<uint16_t>& q, const std::vector<uint16_t>& k,
+                                  const std::vector<uint16_t>& v, const std::vector<uint16_t>& d_out,
+                                  const std::vector<float>& lse, const AttnConfig& cfg) {
+    cfg.validate();
+    if (cfg.dropout_p > 0.0f) throw std::invalid_argument("dropout is not on the B200 path");
+    if (q.size() != cfg.elems() || k.size() != cfg.elems() || v.size() != cfg.elems() ||
+        d_out.size() != cfg.elems())
+        throw std::invalid_argument("backward_fused: input shape mismatch");
+    if (lse.size() != cfg.rows()) throw std::invalid_argument("backward_fused: lse shape mismatch");
+    const int dn = detail::native_dim(cfg.head_dim);
+    const size_t rows = cfg.rows();
+    cudaStream_t s = nullptr;
+    const size_t tb = rows * dn * 2;
+    detail::DevBuf bq(tb), bk(tb), bv(tb), bdo(tb), bo(tb), bdq(tb), bdk(tb), bdv(tb), blse(rows * 4),
+        bjunk(rows * 4);
+    detail::upload_padded(bq.p, q.data(), rows, cfg.head_dim, dn, s);
+    detail::upload_padded(bk.p, k.data(), rows, cfg.head_dim, dn, s);
+    detail::upload_padded(bv.p, v.data(), rows, cfg.head_dim, dn, s);
+    detail::upload_padded(bdo.p, d_out.data(), rows, cfg.head_dim, dn, s);
+    detail::cuda(cudaMemcpyAsync(blse.p, lse.data(), rows * 4, cudaMemcpyHostToDevice, s), "H2D lse");
+    const vattn_config c = detail::to_c(cfg, dn);
+    detail::check(mha_forward(&c, bq.p, bk.p, bv.p, bo.p, static_cast<float*>(bjunk.p), s), "mha_forward");
+    const size_t wsb = mha_backward_workspace_bytes(&c);
+    detail::DevBuf ws(wsb);
+    detail::check(mha_backward(&c, bq.p, bk.p, bv.p, bo.p, bdo.p, static_cast<const float*>(blse.p),
+                               bdq.p, bdk.p, bdv.p, ws.p, wsb, s),
+                  "mha_backward");
+    GradOutputs g;
+    g.dq.resize(cfg.elems());
+    g.dk.resize(cfg.elems());
+    g.dv.resize(cfg.elems());
+    detail::download_padded(g.dq.data(), bdq.p, rows, cfg.head_dim, dn, s);
+    detail::download_padded(g.dk.data(), bdk.p, rows, cfg.head_dim, dn, s);
+    detail::download_padded(g.dv.data(), bdv.p, rows, cfg.head_dim, dn, s);
+    detail::cuda(cudaStreamSynchronize(s), "sync");
+    return g;
+}
+
+}  // namespace vattn_b200

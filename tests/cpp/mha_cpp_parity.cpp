@@ -1,0 +1,122 @@
+// C++ drop-in parity driver (GPU): the same program calls the UNMODIFIED
+// reference library (vattn::, compiled from /root/reference/proj/src into
+// oracle/_ref/libvattn_ref.so -- test infrastructure) and the B200 operator API
+// (vattn_b200::, include/vattn_b200/mha.hpp over libvattn_b200.so) on identical
+// inputs, with the reference's own assertions (proj/tests/test_forward.cpp,
+// test_backward.cpp) restated against the SURVEY 8(c) tolerances.
+// Built by tests/cpp/Makefile; run by tests/test_cpp_api.py.  Exit code = failures.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "vattn/attention.hpp"
+#include "vattn/backward.hpp"
+#include "vattn/reference.hpp"
+#include "vattn/workload.hpp"
+#include "vattn_b200/mha.hpp"
+
+static int g_fail = 0;
+static void check(bool ok, const std::string& what) {
+    std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", what.c_str());
+    if (!ok) ++g_fail;
+}
+
+static std::vector<uint16_t> bits(const vattn::Tensor<vattn::Half>& t) {
+    std::vector<uint16_t> v(t.size());
+    for (size_t i = 0; i < t.size(); ++i) v[i] = t.data()[i].bits;
+    return v;
+}
+
+static vattn::Tensor<double> widen_bits(const std::vector<uint16_t>& b, const std::vector<size_t>& dims) {
+    vattn::Tensor<double> t(dims);
+    for (size_t i = 0; i < b.size(); ++i) t.data()[i] = vattn::f16_to_f32(vattn::Half::from_bits(b[i]));
+    return t;
+}
+
+static bool close(const vattn::Tensor<double>& test, const vattn::Tensor<double>& ref, double fro, double absb,
+                  const std::string& what) {
+    double R = 1.0;
+    for (size_t i = 0; i < ref.size(); ++i) R = std::max(R, std::abs(ref.data()[i]));
+    const double fr = vattn::frobenius_rel_error(test, ref);
+    const double ma = vattn::error_metrics(test, ref).max_abs;
+    std::printf("    %s: fro_rel %.3e  max_abs %.3e (R %.2f)\n", what.c_str(), fr, ma, R);
+    return fr <= fro && ma <= absb * R;
+}
+
+static void run_case(int B, int H, int N, int d, bool causal, uint64_t seed) {
+    const std::vector<size_t> dims{(size_t)B, (size_t)H, (size_t)N, (size_t)d};
+    const auto q = vattn::normal_tensor_f16(seed, 1, dims), k = vattn::normal_tensor_f16(seed, 2, dims),
+               v = vattn::normal_tensor_f16(seed, 3, dims), dout = vattn::normal_tensor_f16(seed, 4, dims);
+    vattn::AttnConfig rc;
+    rc.batch = B; rc.heads = H; rc.seq_len = N; rc.head_dim = d; rc.causal = causal;
+    rc.tile_rows = rc.tile_cols = N < 64 ? N : 64;
+    vattn_b200::AttnConfig bc;
+    bc.batch = B; bc.heads = H; bc.seq_len = N; bc.head_dim = d; bc.causal = causal;
+
+    const auto ref = vattn::attention_ref(vattn::widen(q), vattn::widen(k), vattn::widen(v), rc);
+    const auto fused = vattn::forward_fused(q, k, v, rc);  // reference FP32-ACC fused path
+    const auto ours = vattn_b200::forward_fused(bits(q), bits(k), bits(v), bc);
+    const std::string tag = "B" + std::to_string(B) + " H" + std::to_string(H) + " N" + std::to_string(N) +
+                            " d" + std::to_string(d) + (causal ? " causal" : "");
+    const auto o = widen_bits(ours.out, dims);
+    check(close(o, ref.out, 1e-3, 2e-3, "O vs binary64"), tag + ": O vs attention_ref");
+    check(close(o, vattn::widen(fused.out), 1e-3, 2e-3, "O vs forward_fused"), tag + ": O vs forward_fused FP32-ACC");
+    double lse_rel = 0;
+    for (size_t i = 0; i < ours.lse.size(); ++i)
+        lse_rel = std::max(lse_rel, std::abs(ours.lse[i] - ref.lse.data()[i]) /
+                                        std::max(std::abs(ref.lse.data()[i]), 1.0));
+    check(lse_rel <= 1e-5, tag + ": lse max_rel " + std::to_string(lse_rel) + " <= 1e-5");
+
+    vattn::Tensor<float> lse_t(std::vector<size_t>{(size_t)B, (size_t)H, (size_t)N});
+    for (size_t i = 0; i < ours.lse.size(); ++i) lse_t.data()[i] = ours.lse[i];
+    const auto g = vattn_b200::backward_fused(bits(q), bits(k), bits(v), bits(dout), ours.lse, bc);
+    const auto gr = vattn::attention_grad_ref(vattn::widen(q), vattn::widen(k), vattn::widen(v), vattn::widen(dout), rc);
+    check(close(widen_bits(g.dq, dims), gr.dq, 1e-3, 2e-3, "dQ"), tag + ": dQ vs attention_grad_ref");
+    check(close(widen_bits(g.dk, dims), gr.dk, 1e-3, 2e-3, "dK"), tag + ": dK vs attention_grad_ref");
+    check(close(widen_bits(g.dv, dims), gr.dv, 1e-3, 2e-3, "dV"), tag + ": dV vs attention_grad_ref");
+}
+
+int main() {
+    run_case(1, 2, 128, 64, false, 1);   // BASELINE configs[0]
+    run_case(1, 1, 64, 32, true, 27);    // test_forward.cpp:200-214 (padded d)
+    run_case(2, 3, 64, 20, false, 7);    // test_forward.cpp:54 shape (d=20 padded)
+    run_case(1, 2, 256, 128, true, 3);
+
+    // causal independence is bitwise (test_forward.cpp:182-198) through the C++ API
+    {
+        const std::vector<size_t> dims{1, 1, 64, 16};
+        auto q = vattn::normal_tensor_f16(19, 1, dims), k = vattn::normal_tensor_f16(19, 2, dims),
+             v = vattn::normal_tensor_f16(19, 3, dims);
+        vattn_b200::AttnConfig c;
+        c.seq_len = 64; c.head_dim = 16; c.causal = true;
+        const auto base = vattn_b200::forward_fused(bits(q), bits(k), bits(v), c);
+        auto k2 = bits(k), v2 = bits(v);
+        for (int j = 0; j < 16; ++j) {
+            k2[63 * 16 + j] = vattn::f32_to_f16(9.0f).bits;
+            v2[63 * 16 + j] = vattn::f32_to_f16(-9.0f).bits;
+        }
+        const auto pert = vattn_b200::forward_fused(bits(q), k2, v2, c);
+        bool same = true;
+        for (int i = 0; i < 63 * 16; ++i) same &= pert.out[i] == base.out[i];
+        for (int i = 0; i < 63; ++i) same &= pert.lse[i] == base.lse[i];
+        check(same, "causal independence bitwise (rows 0..62 ignore K/V row 63)");
+    }
+    // error mapping mirrors the reference (std::invalid_argument)
+    {
+        vattn_b200::AttnConfig bad;
+        bad.seq_len = 64; bad.head_dim = 64; bad.dropout_p = 1.0f;
+        bool threw = false;
+        try { bad.validate(); } catch (const std::invalid_argument&) { threw = true; }
+        check(threw, "invalid dropout_p throws std::invalid_argument");
+        vattn_b200::AttnConfig c;
+        c.seq_len = 64; c.head_dim = 64;
+        threw = false;
+        try { vattn_b200::forward_fused(std::vector<uint16_t>(10), std::vector<uint16_t>(10), std::vector<uint16_t>(10), c); }
+        catch (const std::invalid_argument&) { threw = true; }
+        check(threw, "shape mismatch throws std::invalid_argument");
+    }
+    std::printf("%d failure(s)\n", g_fail);
+    return g_fail;
+}
