@@ -269,7 +269,8 @@ extern "C" {
 
 #ifdef VATTN_TRACE
 // Debug-only: select the backward work item to trace / read its timeline.
-int vattn_trace_select(int item) {
+int vattn_trace_select(int kid, int item) {
+    cudaMemcpyToSymbol(g_vattn_trace_kid, &kid, sizeof(int));
     cudaMemcpyToSymbol(g_vattn_trace_block, &item, sizeof(int));
     long long z[4096] = {0};
     cudaMemcpyToSymbol(g_vattn_trace, z, sizeof(z));

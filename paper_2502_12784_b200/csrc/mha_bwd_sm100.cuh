@@ -103,6 +103,8 @@ __global__ void __launch_bounds__(384, 1)
                         const __grid_constant__ CUtensorMap tm_do, void* __restrict__ dk_out,
                         void* __restrict__ dv_out, const BwdParams p) {
     using Cfg = DkdvCfg<kD>;
+    constexpr int kVtraceKid = 1;
+    (void)kVtraceKid;
     using T16 = typename std::conditional<kBF16, __nv_bfloat16, __half>::type;
     constexpr int kSt = Cfg::kStages;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -179,61 +181,63 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp == 1) {
-        // -------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc_kk = umma_idesc_f16(128, 128, kBF16, 0, 0);  // S^T, dP^T
-            constexpr uint32_t idesc_kmn = umma_idesc_f16(128, kD, kBF16, 0, 1);  // dV, dK
-            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aDO = smem_u32(sDO);
-            auto issue_kk = [&](uint32_t dcol, uint32_t abase, uint32_t bbase) {
+        // ------------------------------------------------ MMA issuer (whole warp)
+        constexpr uint32_t idesc_kk = umma_idesc_f16(128, 128, kBF16, 0, 0);  // S^T, dP^T
+        constexpr uint32_t idesc_kmn = umma_idesc_f16(128, kD, kBF16, 0, 1);  // dV, dK
+        constexpr uint64_t kTile16 = Cfg::kTileBytes >> 4;
+        const uint64_t dK = umma_desc_sw128(smem_u32(sK), 16, 1024);
+        const uint64_t dV = umma_desc_sw128(smem_u32(sV), 16, 1024);
+        const uint64_t dQk = umma_desc_sw128(smem_u32(sQ), 16, 1024);       // Q as K-major B
+        const uint64_t dDOk = umma_desc_sw128(smem_u32(sDO), 16, 1024);     // dO as K-major B
+        const uint64_t dQm = umma_desc_sw128(smem_u32(sQ), 16384, 1024);    // Q as MN-major B
+        const uint64_t dDOm = umma_desc_sw128(smem_u32(sDO), 16384, 1024);  // dO as MN-major B
+        auto issue_kk = [&](uint32_t dcol, uint64_t ad, uint64_t bd) {
 #pragma unroll
-                for (int kk = 0; kk < kD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    mma_ss(tmem + dcol, umma_desc_sw128(abase + off, 16, 1024),
-                           umma_desc_sw128(bbase + off, 16, 1024), idesc_kk, kk > 0);
-                }
-            };
-            // A operand (16-bit) held in TMEM by the two warpgroups: queries
-            // [64h, 64h+64) at columns base + 64h + [0, 32).
-            auto issue_ts = [&](uint32_t dcol, uint32_t abase_col, uint32_t bbase, bool acc) {
+            for (int kk = 0; kk < kD / 16; ++kk)
+                mma_ss_e(tmem + dcol, desc_kmajor(ad, kk), desc_kmajor(bd, kk), idesc_kk, kk > 0);
+        };
+        // A operand (16-bit) held in TMEM by the two warpgroups: queries
+        // [64h, 64h+64) at columns base + 64h + [0, 32).
+        auto issue_ts = [&](uint32_t dcol, uint32_t abase_col, uint64_t bd, bool acc) {
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    mma_ts(tmem + dcol, tmem + abase_col + (kk >> 2) * 64 + (kk & 3) * 8,
-                           umma_desc_sw128(bbase + kk * 2048, 16384, 1024), idesc_kmn,
-                           (acc || kk > 0) ? 1u : 0u);
-            };
-            mbar_wait(kv_full, 0);
+            for (int kk = 0; kk < 8; ++kk)
+                mma_ts_e(tmem + dcol, tmem + abase_col + (kk >> 2) * 64 + (kk & 3) * 8, desc_mnmajor(bd, kk),
+                         idesc_kmn, (acc || kk > 0) ? 1u : 0u);
+        };
+        mbar_wait(kv_full, 0);
+        tc_fence_after();
+        mbar_wait(q_full + 0, 0);
+        tc_fence_after();
+        issue_kk(Cfg::kTmemS, dK, dQk);
+        mma_commit_e(s_full);
+        issue_kk(Cfg::kTmemDP, dV, dDOk);
+        mma_commit_e(dp_full);
+        VTRACE(3072);
+        for (int s = 0; s < n_steps; ++s) {
+            const int st = s % kSt;
+            const int st1 = (s + 1) % kSt;
+            mbar_wait(p_full, s & 1);
             tc_fence_after();
-            mbar_wait(q_full + 0, 0);
-            tc_fence_after();
-            issue_kk(Cfg::kTmemS, aK, aQ);
-            mma_commit(s_full);
-            issue_kk(Cfg::kTmemDP, aV, aDO);
-            mma_commit(dp_full);
-            for (int s = 0; s < n_steps; ++s) {
-                const int st = s % kSt;
-                const int st1 = (s + 1) % kSt;
-                const uint32_t qb = aQ + st * Cfg::kTileBytes;
-                const uint32_t dob = aDO + st * Cfg::kTileBytes;
-                mbar_wait(p_full, s & 1);
+            VTRACE(8 * s + 0);
+            issue_ts(Cfg::kTmemDV, Cfg::kTmemS, dDOm + st * kTile16, s > 0);  // dV += P^T dO
+            if (s + 1 < n_steps) {
+                mbar_wait(q_full + st1, ((s + 1) / kSt) & 1);
                 tc_fence_after();
-                issue_ts(Cfg::kTmemDV, Cfg::kTmemS, dob, s > 0);  // dV += P^T dO
-                if (s + 1 < n_steps) {
-                    mbar_wait(q_full + st1, ((s + 1) / kSt) & 1);
-                    tc_fence_after();
-                    issue_kk(Cfg::kTmemS, aK, aQ + st1 * Cfg::kTileBytes);  // in-order after dV read P^T
-                    mma_commit(s_full);
-                }
-                mbar_wait(ds_full, s & 1);
-                tc_fence_after();
-                issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, qb, s > 0);  // dK += dS^T Q
-                mma_commit(q_empty + st);
-                if (s + 1 < n_steps) {
-                    issue_kk(Cfg::kTmemDP, aV, aDO + st1 * Cfg::kTileBytes);  // after dK read dS^T
-                    mma_commit(dp_full);
-                }
+                VTRACE(8 * s + 1);
+                issue_kk(Cfg::kTmemS, dK, dQk + st1 * kTile16);  // in-order after dV read P^T
+                mma_commit_e(s_full);
             }
-            mma_commit(dkv_full);
+            mbar_wait(ds_full, s & 1);
+            tc_fence_after();
+            VTRACE(8 * s + 2);
+            issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0);  // dK += dS^T Q
+            mma_commit_e(q_empty + st);
+            if (s + 1 < n_steps) {
+                issue_kk(Cfg::kTmemDP, dV, dDOk + st1 * kTile16);  // after dK read dS^T
+                mma_commit_e(dp_full);
+            }
         }
+        mma_commit_e(dkv_full);
     } else if (warp >= 4) {
         // ------------------------------------------------------ P / dS warps
         regs_inc<208>();
@@ -251,6 +255,7 @@ __global__ void __launch_bounds__(384, 1)
             mbar_wait(q_full + st, (s / kSt) & 1);  // lse2 / D of this tile landed
             mbar_wait(s_full, s & 1);
             tc_fence_after();
+            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 0);
             float pr[64];
             tmem_ld32f(tmem + lb + Cfg::kTmemS + 64 * h, pr);
             tmem_ld32f(tmem + lb + Cfg::kTmemS + 64 * h + 32, pr + 32);
@@ -278,9 +283,11 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
+            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 1);
 
             mbar_wait(dp_full, s & 1);
             tc_fence_after();
+            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 2);
             uint32_t dsp[32];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -306,6 +313,7 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_arrive(ds_full);
                 mbar_arrive(q_empty + st);  // done with lse2 / D of this stage
             }
+            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 3);
         }
         // ---------------------------------------------------------- epilogue
         mbar_wait(dkv_full, 0);
@@ -380,6 +388,8 @@ __global__ void __launch_bounds__(384, 1)
                       const __grid_constant__ CUtensorMap tm_do,
                       const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
     using Cfg = DqCfg<kD>;
+    constexpr int kVtraceKid = 2;
+    (void)kVtraceKid;
     constexpr int SK = Cfg::kKSlots, SV = Cfg::kVSlots;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem + Cfg::kSmemQ;
@@ -467,64 +477,73 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp == 1) {
-        // -------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc_kk = umma_idesc_f16(128, 128, kBF16, 0, 0);  // S, dP
-            constexpr uint32_t idesc_dq = umma_idesc_f16(128, kD, kBF16, 0, 1);   // dQ (B = K MN-major)
-            const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO), aK = smem_u32(sK), aV = smem_u32(sV);
-            auto kslot = [&](int j) {
-                mbar_wait(k_full + j % SK, (j / SK) & 1);
-                tc_fence_after();
-                return aK + (j % SK) * Cfg::kTileBytes;
-            };
-            auto vslot = [&](int j) {
-                mbar_wait(v_full + j % SV, (j / SV) & 1);
-                tc_fence_after();
-                return aV + (j % SV) * Cfg::kTileBytes;
-            };
-            auto issue_kk = [&](uint32_t dcol, uint32_t abase, uint32_t bbase) {
-#pragma unroll
-                for (int kk = 0; kk < kD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    mma_ss(tmem + dcol, umma_desc_sw128(abase + off, 16, 1024),
-                           umma_desc_sw128(bbase + off, 16, 1024), idesc_kk, kk > 0);
-                }
-            };
-            mbar_wait(qd_full, 0);
+        // ------------------------------------------------ MMA issuer (whole warp)
+        constexpr uint32_t idesc_kk = umma_idesc_f16(128, 128, kBF16, 0, 0);  // S, dP
+        constexpr uint32_t idesc_dq = umma_idesc_f16(128, kD, kBF16, 0, 1);   // dQ (B = K MN-major)
+        constexpr uint64_t kTile16 = Cfg::kTileBytes >> 4;
+        const uint64_t dQd = umma_desc_sw128(smem_u32(sQ), 16, 1024);
+        const uint64_t dDOd = umma_desc_sw128(smem_u32(sDO), 16, 1024);
+        const uint64_t dKk = umma_desc_sw128(smem_u32(sK), 16, 1024);     // K slots, K-major (S)
+        const uint64_t dKm = umma_desc_sw128(smem_u32(sK), 16384, 1024);  // K slots, MN-major (dQ)
+        const uint64_t dVk = umma_desc_sw128(smem_u32(sV), 16, 1024);
+        auto kslot = [&](int j) {
+            mbar_wait(k_full + j % SK, (j / SK) & 1);
             tc_fence_after();
-            issue_kk(0, aQ, kslot(0));  // S_0
-            mma_commit(s_full + 0);
-            issue_kk(Cfg::kTmemDP, aDO, vslot(0));  // dP_0
-            mma_commit(dp_full);
-            mma_commit(v_empty + 0);
-            if (nk > 1) {
-                issue_kk(128, aQ, kslot(1));  // S_1
-                mma_commit(s_full + 1);
-            }
-            for (int j = 0; j < nk; ++j) {
-                const uint32_t R = (j & 1) ? 128u : 0u;
-                const uint32_t kbase = aK + (j % SK) * Cfg::kTileBytes;
-                mbar_wait(ds_full, j & 1);
-                tc_fence_after();
-                // dQ += dS K_j : A = dS in TMEM (warpgroup h: keys [64h, 64h+64) at R + 64h + [0,32))
+            return static_cast<uint64_t>(j % SK) * kTile16;
+        };
+        auto vslot = [&](int j) {
+            mbar_wait(v_full + j % SV, (j / SV) & 1);
+            tc_fence_after();
+            return static_cast<uint64_t>(j % SV) * kTile16;
+        };
+        auto issue_kk = [&](uint32_t dcol, uint64_t ad, uint64_t bd) {
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    mma_ts(tmem + Cfg::kTmemDQ, tmem + R + (kk >> 2) * 64 + (kk & 3) * 8,
-                           umma_desc_sw128(kbase + kk * 2048, 16384, 1024), idesc_dq,
-                           (j > 0 || kk > 0) ? 1u : 0u);
-                mma_commit(k_empty + j % SK);  // K_j consumed (S_j and dQ_j)
-                if (j + 1 < nk) {
-                    issue_kk(Cfg::kTmemDP, aDO, vslot(j + 1));  // dP_(j+1): dS_j already built
-                    mma_commit(dp_full);
-                    mma_commit(v_empty + (j + 1) % SV);
-                }
-                if (j + 2 < nk) {
-                    issue_kk(R, aQ, kslot(j + 2));  // S_(j+2): in-order after dQ_j read dS_j
-                    mma_commit(s_full + (j & 1));
-                }
-            }
-            mma_commit(dq_done);
+            for (int kk = 0; kk < kD / 16; ++kk)
+                mma_ss_e(tmem + dcol, desc_kmajor(ad, kk), desc_kmajor(bd, kk), idesc_kk, kk > 0);
+        };
+        mbar_wait(qd_full, 0);
+        tc_fence_after();
+        issue_kk(0, dQd, dKk + kslot(0));  // S_0
+        mma_commit_e(s_full + 0);
+        issue_kk(Cfg::kTmemDP, dDOd, dVk + vslot(0));  // dP_0
+        mma_commit_e(dp_full);
+        mma_commit_e(v_empty + 0);
+        if (nk > 1) {
+            issue_kk(128, dQd, dKk + kslot(1));  // S_1
+            mma_commit_e(s_full + 1);
         }
+        VTRACE(3072);
+        for (int j = 0; j < nk; ++j) {
+            const uint32_t R = (j & 1) ? 128u : 0u;
+            const uint64_t kd = dKm + static_cast<uint64_t>(j % SK) * kTile16;
+            mbar_wait(ds_full, j & 1);
+            tc_fence_after();
+            VTRACE(8 * j + 0);
+            // dQ += dS K_j : A = dS in TMEM (warpgroup h: keys [64h, 64h+64) at R + 64h + [0,32))
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                mma_ts_e(tmem + Cfg::kTmemDQ, tmem + R + (kk >> 2) * 64 + (kk & 3) * 8, desc_mnmajor(kd, kk),
+                         idesc_dq, (j > 0 || kk > 0) ? 1u : 0u);
+            VTRACE(8 * j + 3);
+            mma_commit_e(k_empty + j % SK);  // K_j consumed (S_j and dQ_j)
+            VTRACE(8 * j + 4);
+            if (j + 1 < nk) {
+                const uint64_t vo = vslot(j + 1);
+                VTRACE(8 * j + 1);
+                issue_kk(Cfg::kTmemDP, dDOd, dVk + vo);  // dP_(j+1): dS_j already built
+                VTRACE(8 * j + 5);
+                mma_commit_e(dp_full);
+                mma_commit_e(v_empty + (j + 1) % SV);
+            }
+            if (j + 2 < nk) {
+                const uint64_t ko = kslot(j + 2);
+                VTRACE(8 * j + 2);
+                issue_kk(R, dQd, dKk + ko);  // S_(j+2): in-order after dQ_j read dS_j
+                VTRACE(8 * j + 6);
+                mma_commit_e(s_full + (j & 1));
+            }
+        }
+        mma_commit_e(dq_done);
     } else if (warp >= 4) {
         regs_inc<208>();
         const int h = (warp - 4) >> 2;           // key-column half
@@ -538,6 +557,7 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t R = (j & 1) ? 128u : 0u;
             mbar_wait(s_full + (j & 1), (j >> 1) & 1);
             tc_fence_after();
+            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 0);
             float pr[64];
             tmem_ld32f(tmem + lb + R + 64 * h, pr);
             tmem_ld32f(tmem + lb + R + 64 * h + 32, pr + 32);
@@ -552,8 +572,10 @@ __global__ void __launch_bounds__(384, 1)
                 const float pv = ex2(fmaf(pr[x], sc, -lse2));
                 pr[x] = x > lim ? 0.0f : pv;
             }
+            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 1);
             mbar_wait(dp_full, j & 1);
             tc_fence_after();
+            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 2);
             uint32_t dsp[32];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -570,6 +592,7 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(ds_full);
+            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 3);
         }
         // ------------------------------------- epilogue: dQ * scale -> 16-bit
         mbar_wait(dq_done, 0);

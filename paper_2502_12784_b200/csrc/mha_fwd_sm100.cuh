@@ -55,6 +55,8 @@ __global__ void __launch_bounds__(384, 1)
                          const __grid_constant__ CUtensorMap tm_v,
                          const __grid_constant__ CUtensorMap tm_o, const FwdParams p) {
     using Cfg = FwdCfg<kD>;
+    constexpr int kVtraceKid = 0;
+    (void)kVtraceKid;
     constexpr int S = Cfg::kStages;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem + Cfg::kSmemQ;
@@ -139,70 +141,70 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp == 1) {
-        // -------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc_s = umma_idesc_f16(128, 128, kBF16, 0, 0);
-            constexpr uint32_t idesc_o = umma_idesc_f16(128, kD, kBF16, 0, 1);
-            const uint32_t sQa = smem_u32(sQ);
-            const uint32_t sKVa = smem_u32(sKV);
-            auto issue_s = [&](int t, int j) {
-                const uint32_t kbase = sKVa + ((2 * j) % S) * Cfg::kTileBytes;
-                const uint32_t qbase = sQa + t * Cfg::kTileBytes;
+        // ------------------------------------------------ MMA issuer (whole warp,
+        // warp-uniform descriptors; one elected lane issues each tcgen05 op)
+        constexpr uint32_t idesc_s = umma_idesc_f16(128, 128, kBF16, 0, 0);
+        constexpr uint32_t idesc_o = umma_idesc_f16(128, kD, kBF16, 0, 1);
+        constexpr uint64_t kTile16 = Cfg::kTileBytes >> 4;
+        const uint64_t dQ0 = umma_desc_sw128(smem_u32(sQ), 16, 1024);      // K-major Q tiles
+        const uint64_t dK0 = umma_desc_sw128(smem_u32(sKV), 16, 1024);     // K-major K slots
+        const uint64_t dV0 = umma_desc_sw128(smem_u32(sKV), 16384, 1024);  // MN-major V slots
+        auto issue_s = [&](int t, int j) {
+            const uint64_t qd = dQ0 + t * kTile16;
+            const uint64_t kd = dK0 + ((2 * j) % S) * kTile16;
 #pragma unroll
-                for (int kk = 0; kk < kD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    mma_ss(tmem + 128 * t, umma_desc_sw128(qbase + off, 16, 1024),
-                           umma_desc_sw128(kbase + off, 16, 1024), idesc_s, kk > 0);
-                }
-                mma_commit(s_full + t);
-            };
-            auto issue_pv = [&](int t, int j) {
-                const uint32_t vbase = sKVa + ((2 * j + 1) % S) * Cfg::kTileBytes;
+            for (int kk = 0; kk < kD / 16; ++kk)
+                mma_ss_e(tmem + 128 * t, desc_kmajor(qd, kk), desc_kmajor(kd, kk), idesc_s, kk > 0);
+            mma_commit_e(s_full + t);
+        };
+        auto issue_pv = [&](int t, int j) {
+            const uint64_t vd = dV0 + ((2 * j + 1) % S) * kTile16;
 #pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    mbar_wait(p_full + 2 * t + hf, j & 1);
-                    tc_fence_after();
-#pragma unroll
-                    for (int k4 = 0; k4 < 4; ++k4) {
-                        const int kk = 4 * hf + k4;
-                        mma_ts(tmem + Cfg::kTmemO + kD * t, tmem + 128 * t + kk * 8,
-                               umma_desc_sw128(vbase + kk * 2048, 16384, 1024), idesc_o,
-                               (j > 0 || kk > 0) ? 1u : 0u);
-                    }
-                }
-                mma_commit(o_done + t);
-            };
-            auto wait_kv = [&](int pos) {
-                mbar_wait(kv_full + (pos % S), (pos / S) & 1);
+            for (int hf = 0; hf < 2; ++hf) {
+                mbar_wait(p_full + 2 * t + hf, j & 1);
                 tc_fence_after();
-            };
-            mbar_wait(q_full, 0);
-            tc_fence_after();
-            if (nkmax > 0) {
-                wait_kv(0);
-                for (int t = 0; t < 2; ++t)
-                    if (nk[t] > 0) issue_s(t, 0);
-                mma_commit(kv_empty + 0);
-            }
-            for (int j = 0; j < nkmax; ++j) {
-                wait_kv(2 * j + 1);
-                bool k_next = false;
 #pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    if (j < nk[t]) {
-                        issue_pv(t, j);
-                        if (j + 1 < nk[t]) {
-                            if (!k_next) {
-                                wait_kv(2 * j + 2);
-                                k_next = true;
-                            }
-                            issue_s(t, j + 1);
+                for (int k4 = 0; k4 < 4; ++k4) {
+                    const int kk = 4 * hf + k4;
+                    mma_ts_e(tmem + Cfg::kTmemO + kD * t, tmem + 128 * t + kk * 8, desc_mnmajor(vd, kk),
+                             idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+                }
+            }
+            mma_commit_e(o_done + t);
+        };
+        auto wait_kv = [&](int pos) {
+            mbar_wait(kv_full + (pos % S), (pos / S) & 1);
+            tc_fence_after();
+        };
+        mbar_wait(q_full, 0);
+        tc_fence_after();
+        VTRACE(3072);
+        if (nkmax > 0) {
+            wait_kv(0);
+            for (int t = 0; t < 2; ++t)
+                if (nk[t] > 0) issue_s(t, 0);
+            mma_commit_e(kv_empty + 0);
+        }
+        for (int j = 0; j < nkmax; ++j) {
+            wait_kv(2 * j + 1);
+            bool k_next = false;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                if (j < nk[t]) {
+                    issue_pv(t, j);
+                    VTRACE(8 * j + 4 * t + 0);
+                    if (j + 1 < nk[t]) {
+                        if (!k_next) {
+                            wait_kv(2 * j + 2);
+                            k_next = true;
                         }
+                        VTRACE(8 * j + 4 * t + 1);
+                        issue_s(t, j + 1);
                     }
                 }
-                mma_commit(kv_empty + (2 * j + 1) % S);
-                if (k_next) mma_commit(kv_empty + (2 * j + 2) % S);
             }
+            mma_commit_e(kv_empty + (2 * j + 1) % S);
+            if (k_next) mma_commit_e(kv_empty + (2 * j + 2) % S);
         }
     } else if (warp >= 4) {
         // ----------------------------------------------------------- softmax
@@ -220,6 +222,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int j = 0; j < ntile; ++j) {
             mbar_wait(s_full + t, j & 1);
             tc_fence_after();
+            if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 0);
             float s[128];
             tmem_ld32f(tS + 0, s);
             tmem_ld32f(tS + 32, s + 32);
@@ -280,6 +283,7 @@ __global__ void __launch_bounds__(384, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(p_full + 2 * t + c);
+                if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 1 + c);
             }
         }
         if (ntile > 0) {

@@ -183,6 +183,49 @@ VATTN_DEV void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_
         : "memory");
 }
 
+// Warp-uniform variants: the whole warp executes them (so descriptors stay in
+// uniform registers) and one elected lane issues the instruction.
+VATTN_DEV void mma_ss_e(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+VATTN_DEV void mma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+VATTN_DEV void mma_commit_e(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+// Descriptor of the kk-th K=16 slice of a 128-row SW128 operand tile whose base
+// descriptor is `d0` (address field counts 16-byte units; no carry possible
+// below 256 KB of shared memory).
+//  K-major  (rows = M/N, 64 K-elements per 128-B row, 16 KB per 64-col box)
+VATTN_DEV uint64_t desc_kmajor(uint64_t d0, int kk) {
+    return d0 + static_cast<uint64_t>(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+}
+//  MN-major (rows = K, 16 K-rows = 2048 B per slice)
+VATTN_DEV uint64_t desc_mnmajor(uint64_t d0, int kk) { return d0 + static_cast<uint64_t>((kk * 2048) >> 4); }
+
 // Arrive on `bar` once every previously issued tcgen05.mma of this thread completes.
 VATTN_DEV void mma_commit(uint64_t* bar) {
     asm volatile(
@@ -295,10 +338,12 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t M, uint32_t N, ui
 #ifdef VATTN_TRACE
 __device__ long long g_vattn_trace[4096];
 __device__ int g_vattn_trace_block;
-#define VTRACE(slot)                                                                  \
-    do {                                                                             \
-        if (static_cast<int>(blockIdx.x + blockIdx.y * gridDim.x) == g_vattn_trace_block) \
-            g_vattn_trace[(slot)] = clock64();                                       \
+__device__ int g_vattn_trace_kid;  // which kernel (kVtraceKid of the kernel) is traced
+#define VTRACE(slot)                                                                      \
+    do {                                                                                 \
+        if (kVtraceKid == g_vattn_trace_kid &&                                            \
+            static_cast<int>(blockIdx.x + blockIdx.y * gridDim.x) == g_vattn_trace_block) \
+            g_vattn_trace[(slot)] = clock64();                                           \
     } while (0)
 #else
 #define VTRACE(slot) \

@@ -1,7 +1,8 @@
-"""Timeline of one backward CTA (debug build tools/libvattn_b200_trace.so).
+"""Timelines of one CTA of each kernel (debug build tools/libvattn_b200_trace.so).
 
-usage: python tools/trace_bwd.py B H N d causal item
-Prints, per query-tile step, the clock64 deltas between pipeline events.
+usage: python tools/trace_bwd.py B H N d causal [block]
+Prints per-iteration clock64 stamps (relative to the MMA loop start) for the
+forward, dK/dV and dQ kernels of the same problem.
 """
 import ctypes as C
 import os
@@ -12,10 +13,11 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import paper_2502_12784_b200 as vb  # noqa: E402  (for the config struct)
+import paper_2502_12784_b200 as vb  # noqa: E402  (config struct only)
 
 lib = C.CDLL(os.path.join(ROOT, "tools", "libvattn_b200_trace.so"))
-B, H, N, d, causal, item = (int(x) for x in sys.argv[1:7])
+B, H, N, d, causal = (int(x) for x in sys.argv[1:6])
+block = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 dt = torch.bfloat16
 q, k, v, do = (torch.randn(B, H, N, d, device="cuda").to(dt) for _ in range(4))
 o = torch.empty_like(q)
@@ -29,7 +31,10 @@ lib.mha_backward_workspace_bytes.restype = C.c_size_t
 ws = torch.empty(lib.mha_backward_workspace_bytes(C.byref(cfg)), dtype=torch.uint8, device="cuda")
 dq, dk, dv = (torch.empty_like(q) for _ in range(3))
 s = torch.cuda.current_stream().cuda_stream
-assert lib.mha_forward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(), s) == 0
+
+
+def fwd():
+    assert lib.mha_forward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(), s) == 0
 
 
 def bwd():
@@ -38,32 +43,40 @@ def bwd():
 
 
 for _ in range(3):
+    fwd()
     bwd()
 torch.cuda.synchronize()
-lib.vattn_trace_select(item)
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-bwd()
-e1.record()
-torch.cuda.synchronize()
-print(f"bwd total {e0.elapsed_time(e1):.3f} ms")
-buf = (C.c_longlong * 4096)()
-lib.vattn_trace_read(buf, 4096)
-t = np.array(buf[:], dtype=np.int64)
-t0 = t[3072]
+
+
+def trace(kid, fn):
+    lib.vattn_trace_select(kid, block)
+    fn()
+    torch.cuda.synchronize()
+    buf = (C.c_longlong * 4096)()
+    lib.vattn_trace_read(buf, 4096)
+    return np.array(buf[:], dtype=np.int64)
+
+
+def show(t, names_m, names_w, n_iter, width):
+    t0 = t[3072]
+    print("iter | MMA: " + " ".join(f"{x:>9}" for x in names_m) + " | WG: " + " ".join(f"{x:>9}" for x in names_w) + " | dt")
+    prev = None
+    for it in range(n_iter):
+        m = [t[width * it + j] - t0 if t[width * it + j] else -1 for j in range(len(names_m))]
+        w = [t[1024 + width * it + j] - t0 if t[1024 + width * it + j] else -1 for j in range(len(names_w))]
+        dtv = (m[0] - prev) if prev is not None and m[0] >= 0 else 0
+        prev = m[0] if m[0] >= 0 else prev
+        print(f"{it:4d} | " + " ".join(f"{x:9d}" for x in m) + " | " + " ".join(f"{x:9d}" for x in w) + f" | {dtv}")
+
+
 n_q = (N + 127) // 128
-kb = item % n_q
-steps = (n_q - kb) if causal else n_q
-print(f"item {item} kb {kb} steps {steps}; cycles relative to CTA start")
-names_m = ["p_full", "dq_empty", "q_next", "ds_full", "dQ_iss"]
-names_s = ["s_full", "P_done", "dp_full", "ds_free", "dS_done"]
-names_q = ["sem_ok", "dq_full", "written", "released"]
-print("step | MMA: " + " ".join(f"{x:>8}" for x in names_m) + " | dS: " + " ".join(f"{x:>8}" for x in names_s) +
-      " | dQ: " + " ".join(f"{x:>8}" for x in names_q))
-prev = None
-for st in range(steps):
-    m = [t[8 * st + j] - t0 if t[8 * st + j] else -1 for j in range(5)]
-    sx = [t[1024 + 8 * st + j] - t0 if t[1024 + 8 * st + j] else -1 for j in range(5)]
-    qx = [t[2048 + 8 * st + j] - t0 if t[2048 + 8 * st + j] else -1 for j in range(4)]
-    print(f"{st:4d} | " + " ".join(f"{x:8d}" for x in m) + " | " + " ".join(f"{x:8d}" for x in sx) + " | " +
-          " ".join(f"{x:8d}" for x in qx))
+if "dq" not in sys.argv:
+    print(f"== forward, block {block}")
+    t = trace(0, fwd)
+    show(t, ["pv0", "s0next", "-", "-", "pv1", "s1next"], ["s0", "p0a", "p0b", "-", "s1", "p1a", "p1b"], min(n_q, 24), 8)
+    print(f"== dK/dV, block {block}")
+    t = trace(1, bwd)
+    show(t, ["p_full", "q_next", "ds_full"], ["s_full", "P_done", "dp_full", "dS_done"], min(n_q, 24), 8)
+print(f"== dQ, block {block}")
+t = trace(2, bwd)
+show(t, ["ds_full", "v_next", "k_next2", "dQ_iss", "commit", "dP_iss", "S_iss"], ["s_full", "P_done", "dp_full", "dS_done"], min(n_q, 24), 8)
