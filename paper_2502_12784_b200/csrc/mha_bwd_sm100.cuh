@@ -261,17 +261,21 @@ __global__ void __launch_bounds__(384, 1)
             tmem_ld32f(tmem + lb + Cfg::kTmemS + 64 * h + 32, pr + 32);
             tmem_wait_ld();
             const int qbase = i * 128 + 64 * h;
-            const bool diag = p.causal && i == kb;
 #pragma unroll
             for (int x = 0; x < 64; x += 4) {
                 const float4 l4 = *reinterpret_cast<const float4*>(lse2 + x);
-                const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+                pr[x + 0] = ex2(fmaf(pr[x + 0], sc, -l4.x));
+                pr[x + 1] = ex2(fmaf(pr[x + 1], sc, -l4.y));
+                pr[x + 2] = ex2(fmaf(pr[x + 2], sc, -l4.z));
+                pr[x + 3] = ex2(fmaf(pr[x + 3], sc, -l4.w));
+            }
+            // masks only on the (warp-uniform) diagonal tile / the last key tile
+            if ((p.causal && i == kb) || kb * 128 + 128 > N) {
+                // P = 0 for columns x < lim: key > query on the diagonal, all for keys >= N
+                const int lim = !key_ok ? 64 : ((p.causal && i == kb) ? key - qbase : 0);
 #pragma unroll
-                for (int y = 0; y < 4; ++y) {
-                    float pv = ex2(fmaf(pr[x + y], sc, -lv[y]));
-                    if (!key_ok || (diag && key > qbase + x + y)) pv = 0.0f;
-                    pr[x + y] = pv;
-                }
+                for (int x = 0; x < 64; ++x)
+                    if (x < lim) pr[x] = 0.0f;
             }
             {
                 uint32_t pk[32];
@@ -527,10 +531,12 @@ __global__ void __launch_bounds__(384, 1)
             VTRACE(8 * j + 3);
             mma_commit_e(k_empty + j % SK);  // K_j consumed (S_j and dQ_j)
             VTRACE(8 * j + 4);
+            // dP_(j+1) after dQ_j (measured: issuing it first delays S_(j+2) and the
+            // next P pass more than it shortens the dS chain)
             if (j + 1 < nk) {
                 const uint64_t vo = vslot(j + 1);
                 VTRACE(8 * j + 1);
-                issue_kk(Cfg::kTmemDP, dDOd, dVk + vo);  // dP_(j+1): dS_j already built
+                issue_kk(Cfg::kTmemDP, dDOd, dVk + vo);
                 VTRACE(8 * j + 5);
                 mma_commit_e(dp_full);
                 mma_commit_e(v_empty + (j + 1) % SV);

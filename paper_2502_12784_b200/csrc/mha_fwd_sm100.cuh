@@ -238,9 +238,16 @@ __global__ void __launch_bounds__(384, 1)
                 for (int c = 0; c < 128; ++c)
                     if (c > lim) s[c] = -INFINITY;
             }
-            float mx = s[0];
+            // tree reduction (8 independent chains) instead of a 128-deep dependency chain
+            float mx8[8];
 #pragma unroll
-            for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+            for (int u = 0; u < 8; ++u) mx8[u] = s[u];
+#pragma unroll
+            for (int c = 8; c < 128; c += 8)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], s[c + u]);
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
             const float m_tile = mx * sc;
             if (j == 0) {
                 m_run = m_tile;
@@ -269,6 +276,7 @@ __global__ void __launch_bounds__(384, 1)
             const float m_use = m_run == -INFINITY ? 0.0f : m_run;
             // P in two halves (keys [0,64) then [64,128)): the MMA warp starts the
             // first half of P V while the second half is still being exponentiated.
+            float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // independent partial row sums
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 uint32_t pk[32];
@@ -276,7 +284,7 @@ __global__ void __launch_bounds__(384, 1)
                 for (int x = 0; x < 32; ++x) {
                     const float p0 = ex2(fmaf(s[64 * c + 2 * x], sc, -m_use));
                     const float p1 = ex2(fmaf(s[64 * c + 2 * x + 1], sc, -m_use));
-                    l_run += p0 + p1;
+                    ls[x & 3] += p0 + p1;
                     pk[x] = pack2<kBF16>(p0, p1);
                 }
                 tmem_st32(tS + 32 * c, pk);
@@ -285,6 +293,7 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_arrive(p_full + 2 * t + c);
                 if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 1 + c);
             }
+            l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         }
         if (ntile > 0) {
             // ------------------------------------------------------ epilogue
