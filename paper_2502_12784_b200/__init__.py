@@ -34,7 +34,7 @@ __all__ = [
     "workspace_bytes", "MHAFunction", "attention", "LIB_PATH", "lib",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvattn_b200.so")
+LIB_PATH = os.environ.get("VATTN_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvattn_b200.so")
 
 VATTN_OK, VATTN_EINVAL, VATTN_EDOMAIN, VATTN_EUNSUPPORTED, VATTN_ECUDA = range(5)
 VATTN_F16, VATTN_BF16 = 0, 1

@@ -461,14 +461,14 @@ __global__ void __launch_bounds__(384, 1)
             // K runs ahead of V (S_(j+1) is issued before dP_(j+1))
             auto load_k = [&](int j) {
                 const int sl = j % SK;
-                mbar_wait(k_empty + sl, ((j / SK) & 1) ^ 1);
+                mbar_wait<VATTN_SLEEP_PRODUCER>(k_empty + sl, ((j / SK) & 1) ^ 1);
                 mbar_arrive_expect_tx(k_full + sl, Cfg::kTileBytes);
                 for (int b = 0; b < Cfg::kBoxes; ++b)
                     tma_load_3d(sK + sl * Cfg::kTileBytes + b * 16384, &tm_k, k_full + sl, b * 64, j * 128, bh);
             };
             auto load_v = [&](int j) {
                 const int sl = j % SV;
-                mbar_wait(v_empty + sl, ((j / SV) & 1) ^ 1);
+                mbar_wait<VATTN_SLEEP_PRODUCER>(v_empty + sl, ((j / SV) & 1) ^ 1);
                 mbar_arrive_expect_tx(v_full + sl, Cfg::kTileBytes);
                 for (int b = 0; b < Cfg::kBoxes; ++b)
                     tma_load_3d(sV + sl * Cfg::kTileBytes + b * 16384, &tm_v, v_full + sl, b * 64, j * 128, bh);
@@ -491,12 +491,12 @@ __global__ void __launch_bounds__(384, 1)
         const uint64_t dKm = umma_desc_sw128(smem_u32(sK), 16384, 1024);  // K slots, MN-major (dQ)
         const uint64_t dVk = umma_desc_sw128(smem_u32(sV), 16, 1024);
         auto kslot = [&](int j) {
-            mbar_wait(k_full + j % SK, (j / SK) & 1);
+            mbar_wait_mma(k_full + j % SK, (j / SK) & 1);
             tc_fence_after();
             return static_cast<uint64_t>(j % SK) * kTile16;
         };
         auto vslot = [&](int j) {
-            mbar_wait(v_full + j % SV, (j / SV) & 1);
+            mbar_wait_mma(v_full + j % SV, (j / SV) & 1);
             tc_fence_after();
             return static_cast<uint64_t>(j % SV) * kTile16;
         };
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int kk = 0; kk < kD / 16; ++kk)
                 mma_ss_e(tmem + dcol, desc_kmajor(ad, kk), desc_kmajor(bd, kk), idesc_kk, kk > 0);
         };
-        mbar_wait(qd_full, 0);
+        mbar_wait_mma(qd_full, 0);
         tc_fence_after();
         issue_kk(0, dQd, dKk + kslot(0));  // S_0
         mma_commit_e(s_full + 0);
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int j = 0; j < nk; ++j) {
             const uint32_t R = (j & 1) ? 128u : 0u;
             const uint64_t kd = dKm + static_cast<uint64_t>(j % SK) * kTile16;
-            mbar_wait(ds_full, j & 1);
+            mbar_wait_mma(ds_full, j & 1);
             tc_fence_after();
             VTRACE(8 * j + 0);
             // dQ += dS K_j : A = dS in TMEM (warpgroup h: keys [64h, 64h+64) at R + 64h + [0,32))
@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(384, 1)
         const float dsum = p.dsum[static_cast<size_t>(bh) * p.Npad + q];
         for (int j = 0; j < nk; ++j) {
             const uint32_t R = (j & 1) ? 128u : 0u;
-            mbar_wait(s_full + (j & 1), (j >> 1) & 1);
+            mbar_wait<VATTN_SLEEP_MATH>(s_full + (j & 1), (j >> 1) & 1);
             tc_fence_after();
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 0);
             float pr[64];
@@ -575,11 +575,11 @@ __global__ void __launch_bounds__(384, 1)
             lim = min(lim, N - 1 - kbase);
 #pragma unroll
             for (int x = 0; x < 64; ++x) {
-                const float pv = ex2(fmaf(pr[x], sc, -lse2));
+                const float pv = ex2_mix<VATTN_POLY_DQ>(x / 2, fmaf(pr[x], sc, -lse2));
                 pr[x] = x > lim ? 0.0f : pv;
             }
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 1);
-            mbar_wait(dp_full, j & 1);
+            mbar_wait<VATTN_SLEEP_MATH>(dp_full, j & 1);
             tc_fence_after();
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 2);
             uint32_t dsp[32];
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(384, 1)
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 3);
         }
         // ------------------------------------- epilogue: dQ * scale -> 16-bit
-        mbar_wait(dq_done, 0);
+        mbar_wait<VATTN_SLEEP_MATH>(dq_done, 0);
         tc_fence_after();
         uint8_t* sOut = sQ;  // Q tile is dead once the last S landed
 #pragma unroll

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(384, 1)
                     const int pos = 2 * j + w;
                     const int slot = pos % S;
                     const uint32_t ph = (pos / S) & 1;
-                    mbar_wait(kv_empty + slot, ph ^ 1);
+                    mbar_wait<VATTN_SLEEP_PRODUCER>(kv_empty + slot, ph ^ 1);
                     mbar_arrive_expect_tx(kv_full + slot, Cfg::kTileBytes);
                     uint8_t* dst = sKV + slot * Cfg::kTileBytes;
                     const CUtensorMap* map = w == 0 ? &tm_k : &tm_v;
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(384, 1)
             const uint64_t vd = dV0 + ((2 * j + 1) % S) * kTile16;
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
-                mbar_wait(p_full + 2 * t + hf, j & 1);
+                mbar_wait_mma(p_full + 2 * t + hf, j & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int k4 = 0; k4 < 4; ++k4) {
@@ -173,10 +173,10 @@ __global__ void __launch_bounds__(384, 1)
             mma_commit_e(o_done + t);
         };
         auto wait_kv = [&](int pos) {
-            mbar_wait(kv_full + (pos % S), (pos / S) & 1);
+            mbar_wait_mma(kv_full + (pos % S), (pos / S) & 1);
             tc_fence_after();
         };
-        mbar_wait(q_full, 0);
+        mbar_wait_mma(q_full, 0);
         tc_fence_after();
         VTRACE(3072);
         if (nkmax > 0) {
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(384, 1)
         float l_run = 0.0f;
         const int ntile = nk[t];
         for (int j = 0; j < ntile; ++j) {
-            mbar_wait(s_full + t, j & 1);
+            mbar_wait<VATTN_SLEEP_MATH>(s_full + t, j & 1);
             tc_fence_after();
             if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 0);
             float s[128];
@@ -229,26 +229,28 @@ __global__ void __launch_bounds__(384, 1)
             tmem_ld32f(tS + 64, s + 64);
             tmem_ld32f(tS + 96, s + 96);
             tmem_wait_ld();
-            // masking: causal diagonal tile (keys > row) or keys beyond N
+            if ((warp & 3) == 0 && lane == 0) VTRACE(2048 + 8 * j + 4 * t + 0);
+            // (tile-uniform) masking: causal diagonal tile (keys > row) or keys beyond N
+            const bool tile_masked = p.causal ? (j == ntile - 1) : (j == p.n_kv - 1 && (N & 127) != 0);
             int lim = 127;
             if (p.causal && j == ntile - 1) lim = r;  // diagonal: j*128 == tile row base
             if (!p.causal && j == p.n_kv - 1) lim = min(lim, N - j * 128 - 1);
-            if (lim < 127) {
+            if (tile_masked) {
 #pragma unroll
                 for (int c = 0; c < 128; ++c)
                     if (c > lim) s[c] = -INFINITY;
             }
             // tree reduction (8 independent chains) instead of a 128-deep dependency chain
-            float mx8[8];
+            float mx64[64];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) mx8[u] = s[u];
+            for (int u = 0; u < 64; ++u) mx64[u] = fmax_nr(s[u], s[u + 64]);
 #pragma unroll
-            for (int c = 8; c < 128; c += 8)
+            for (int w = 32; w >= 1; w >>= 1)
 #pragma unroll
-                for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], s[c + u]);
-            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+                for (int u = 0; u < w; ++u) mx64[u] = fmax_nr(mx64[u], mx64[u + w]);
+            const float mx = mx64[0];
             const float m_tile = mx * sc;
+            if ((warp & 3) == 0 && lane == 0) VTRACE(2048 + 8 * j + 4 * t + 1);
             if (j == 0) {
                 m_run = m_tile;
             } else if (__any_sync(0xffffffffu, m_tile > m_run + 8.0f)) {
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(384, 1)
                     m_run = m_tile;
                 }
                 l_run *= f;
-                mbar_wait(o_done + t, (j - 1) & 1);
+                mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (j - 1) & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < kD / 32; ++c) {
@@ -274,16 +276,16 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
             const float m_use = m_run == -INFINITY ? 0.0f : m_run;
+            if ((warp & 3) == 0 && lane == 0) VTRACE(2048 + 8 * j + 4 * t + 2);
+            float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // independent partial row sums
             // P in two halves (keys [0,64) then [64,128)): the MMA warp starts the
             // first half of P V while the second half is still being exponentiated.
-            float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // independent partial row sums
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
+            auto emit_half = [&](int c, auto exp2f_) {
                 uint32_t pk[32];
 #pragma unroll
                 for (int x = 0; x < 32; ++x) {
-                    const float p0 = ex2(fmaf(s[64 * c + 2 * x], sc, -m_use));
-                    const float p1 = ex2(fmaf(s[64 * c + 2 * x + 1], sc, -m_use));
+                    const float p0 = exp2f_(x, fmaf(s[64 * c + 2 * x], sc, -m_use));
+                    const float p1 = exp2f_(x, fmaf(s[64 * c + 2 * x + 1], sc, -m_use));
                     ls[x & 3] += p0 + p1;
                     pk[x] = pack2<kBF16>(p0, p1);
                 }
@@ -292,12 +294,21 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_before();
                 mbar_arrive(p_full + 2 * t + c);
                 if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 1 + c);
+            };
+            auto ex2_fast = [](int x, float v) { return ex2_mix<VATTN_POLY_FWD>(x, v); };
+            auto ex2_exact = [](int, float v) { return ex2(v); };  // -inf -> exact 0
+            if (tile_masked) {  // warp-uniform: tcgen05.st below is .sync.aligned
+                emit_half(0, ex2_exact);
+                emit_half(1, ex2_exact);
+            } else {
+                emit_half(0, ex2_fast);
+                emit_half(1, ex2_fast);
             }
             l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         }
         if (ntile > 0) {
             // ------------------------------------------------------ epilogue
-            mbar_wait(o_done + t, (ntile - 1) & 1);
+            mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (ntile - 1) & 1);
             tc_fence_after();
             const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
             if (row < N) {

@@ -66,6 +66,22 @@ VATTN_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     return ok != 0;
 }
 
+// try_wait with a suspend-time hint: the thread is parked in hardware until the
+// phase completes (or the hint elapses) instead of spinning, so a long-waiting
+// warp does not steal issue slots from the math warps of its SM sub-partition
+// (at the price of a slower wake-up: use it off the critical path).
+VATTN_DEV bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+    return ok != 0;
+}
+
 VATTN_DEV uint64_t globaltimer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -78,24 +94,67 @@ VATTN_DEV uint64_t globaltimer_ns() {
 #define VATTN_WATCHDOG_NS 20000000000ull
 #endif
 
-// Wait until the phase with parity `parity` has completed.
-VATTN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+// MMA-warp wait flavour (experiment knob): 0 spin, 1 spin with nanosleep backoff,
+// 2 short suspend hint.
+#ifndef VATTN_MMA_WAIT
+#define VATTN_MMA_WAIT 1
+#endif
+VATTN_DEV bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+    return ok != 0;
+}
+VATTN_DEV void mbar_wait_mma(uint64_t* bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t n = 0;
+    while (true) {
+#if VATTN_MMA_WAIT == 2
+        if (mbar_try_wait_hint(bar, parity, 200u)) return;
+#else
+        if (mbar_try_wait(bar, parity)) return;
+#if VATTN_MMA_WAIT == 1
+        __nanosleep(20);
+#endif
+#endif
+        if ((++n & 255u) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) __trap();
+    }
+}
+
+// Wait until the phase with parity `parity` has completed (kSleep: park instead of spin).
+template <bool kSleep = false>
+VATTN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+    auto probe = [&] { return kSleep ? mbar_try_wait_sleep(bar, parity) : mbar_try_wait(bar, parity); };
+    if (probe()) return;
 #if VATTN_WATCHDOG_NS
     const uint64_t t0 = globaltimer_ns();
     uint32_t n = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) {
+    while (!probe()) {
+        if ((++n & (kSleep ? 0u : 1023u)) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) {
             printf("vattn watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n",
                    (int)(blockIdx.x + blockIdx.y * gridDim.x), (int)threadIdx.x, smem_u32(bar), parity);
             __trap();
         }
     }
 #else
-    while (!mbar_try_wait(bar, parity)) {
+    while (!probe()) {
     }
 #endif
 }
+
+// Role-specific wait policy (bit set = that role parks instead of spinning).
+#ifndef VATTN_SLEEP_MASK
+#define VATTN_SLEEP_MASK 1
+#endif
+#define VATTN_SLEEP_PRODUCER ((VATTN_SLEEP_MASK & 1) != 0)
+#define VATTN_SLEEP_MMA ((VATTN_SLEEP_MASK & 2) != 0)
+#define VATTN_SLEEP_MATH ((VATTN_SLEEP_MASK & 4) != 0)
 
 // -------------------------------------------------------------------- TMA --
 
@@ -378,6 +437,47 @@ VATTN_DEV float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// 2^x on the FMA pipe (degree-4 minimax on [-0.5, 0.5], max rel. error 2.9e-6):
+// relieves the MUFU (16 ex2/clk/SM), which every P pass of this path saturates.
+// x is clamped at -127 (result ~1e-38, i.e. a zero contribution); +inf never occurs.
+VATTN_DEV float ex2_poly(float x) {
+    x = fmaxf(x, -127.0f);
+    const float t = x + 12582912.0f;  // 1.5 * 2^23: round(x) lands in the low mantissa bits
+    const float f = x - (t - 12582912.0f);
+    float p = fmaf(f, 0.009582852944731712f, 0.055906426161527634f);
+    p = fmaf(p, f, 0.24024099111557007f);
+    p = fmaf(p, f, 0.6931241750717163f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// Share of exponentials routed to ex2_poly: element pairs with pair % period == 0
+// (period 0 = MUFU only).  Tuned per kernel on B200 (bench.py, C3).
+#ifndef VATTN_POLY_FWD
+#define VATTN_POLY_FWD 0
+#endif
+#ifndef VATTN_POLY_DKDV
+#define VATTN_POLY_DKDV 4
+#endif
+#ifndef VATTN_POLY_DQ
+#define VATTN_POLY_DQ 0
+#endif
+// `pair` is an unrolled loop index, so the branch folds away at compile time.
+template <int kPeriod>
+VATTN_DEV float ex2_mix(int pair, float x) {
+    if constexpr (kPeriod > 0) {
+        if (pair % kPeriod == 0) return ex2_poly(x);
+    }
+    return ex2(x);
+}
+
+// fmax the compiler cannot re-associate into one dependent FMNMX3 chain
+VATTN_DEV float fmax_nr(float a, float b) {
+    float r;
+    asm("max.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
 }
 
 VATTN_DEV float lg2(float x) {

@@ -74,9 +74,13 @@ if "dq" not in sys.argv:
     print(f"== forward, block {block}")
     t = trace(0, fwd)
     show(t, ["pv0", "s0next", "-", "-", "pv1", "s1next"], ["s0", "p0a", "p0b", "-", "s1", "p1a", "p1b"], min(n_q, 24), 8)
+    print("softmax tile0: ldtm_done max_done rescale_done (relative to s0)")
+    for it in range(min(n_q, 8)):
+        s0 = t[1024 + 8 * it]
+        print(it, [int(t[2048 + 8 * it + k] - s0) for k in range(3)], "p0a", int(t[1024 + 8 * it + 1] - s0), "p0b", int(t[1024 + 8 * it + 2] - s0))
     print(f"== dK/dV, block {block}")
     t = trace(1, bwd)
-    show(t, ["p_full", "q_next", "ds_full"], ["s_full", "P_done", "dp_full", "dS_done"], min(n_q, 24), 8)
+    show(t, ["p_full", "S_next", "ds_full"], ["s_full", "P_done", "dp_full", "dS_done"], min(n_q, 24), 8)
 print(f"== dQ, block {block}")
 t = trace(2, bwd)
 show(t, ["ds_full", "v_next", "k_next2", "dQ_iss", "commit", "dP_iss", "S_iss"], ["s_full", "P_done", "dp_full", "dS_done"], min(n_q, 24), 8)

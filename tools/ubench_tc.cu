@@ -118,6 +118,24 @@ __global__ void __launch_bounds__(64, 1) latency_bench(long long* out, int reps)
     if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+// MUFU ex2 throughput: each thread runs 8 independent ex2 chains.
+__global__ void __launch_bounds__(512) ex2_bench(long long* out, int reps) {
+    float v[8];
+    for (int i = 0; i < 8; ++i) v[i] = -0.001f * (threadIdx.x + i);
+    __syncthreads();
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = ex2(v[i]) - 1.0f;
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    float acc = 0;
+    for (int i = 0; i < 8; ++i) acc += v[i];
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    if (acc == 1234.5f) out[1000] = 1;
+}
+
 template <typename K>
 double run(K kern, int grid, int block, int smem, int reps) {
     long long* d;
@@ -148,6 +166,21 @@ int main(int argc, char** argv) {
     if (which == 3) report("TS N=64", run(mma_bench<64, true>, 148, 128, 131072, reps), 64);
     if (which == 4) report("TS N=128", run(mma_bench<128, true>, 148, 128, 131072, reps), 128);
     if (which == 5) report("TS N=256", run(mma_bench<256, true>, 148, 128, 131072, reps), 256);
+    if (which == 7) {
+        for (int threads : {128, 256, 512}) {
+            long long* d;
+            cudaMalloc(&d, 2000 * 8);
+            ex2_bench<<<148, threads>>>(d, reps);
+            ex2_bench<<<148, threads>>>(d, reps);
+            cudaDeviceSynchronize();
+            long long h;
+            cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+            printf("ex2: %d threads/SM x %d ex2 in %lld cyc -> %.2f ex2/clk/SM\n", threads, reps * 8, h,
+                   double(threads) * reps * 8 / h);
+            cudaFree(d);
+        }
+        return 0;
+    }
     if (which != 6) return 0;
     const double ld = run(ldtm_bench, 148, 128, 0, reps);
     printf("LDTM 4 warps x 4 x ld32 (64 KB): %.1f cyc per 64 KB -> %.1f B/clk/SM\n", ld / reps, 65536.0 * reps / ld);
