@@ -264,8 +264,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
             for (int x = 0; x < 64; x += 4) {
                 const float4 l4 = *reinterpret_cast<const float4*>(lse2 + x);
-                pr[x + 0] = ex2(fmaf(pr[x + 0], sc, -l4.x));
-                pr[x + 1] = ex2(fmaf(pr[x + 1], sc, -l4.y));
+                pr[x + 0] = ex2_mix<PolyPeriod<kD>::dkdv>(x / 2, fmaf(pr[x + 0], sc, -l4.x));
+                pr[x + 1] = ex2_mix<PolyPeriod<kD>::dkdv>(x / 2, fmaf(pr[x + 1], sc, -l4.y));
                 pr[x + 2] = ex2(fmaf(pr[x + 2], sc, -l4.z));
                 pr[x + 3] = ex2(fmaf(pr[x + 3], sc, -l4.w));
             }
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(384, 1)
             lim = min(lim, N - 1 - kbase);
 #pragma unroll
             for (int x = 0; x < 64; ++x) {
-                const float pv = ex2_mix<VATTN_POLY_DQ>(x / 2, fmaf(pr[x], sc, -lse2));
+                const float pv = ex2_mix<PolyPeriod<kD>::dq>(x / 2, fmaf(pr[x], sc, -lse2));
                 pr[x] = x > lim ? 0.0f : pv;
             }
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 1);

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_arrive(p_full + 2 * t + c);
                 if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 1 + c);
             };
-            auto ex2_fast = [](int x, float v) { return ex2_mix<VATTN_POLY_FWD>(x, v); };
+            auto ex2_fast = [](int x, float v) { return ex2_mix<PolyPeriod<kD>::fwd>(x, v); };
             auto ex2_exact = [](int, float v) { return ex2(v); };  // -inf -> exact 0
             if (tile_masked) {  // warp-uniform: tcgen05.st below is .sync.aligned
                 emit_half(0, ex2_exact);

@@ -459,11 +459,27 @@ VATTN_DEV float ex2_poly(float x) {
 #define VATTN_POLY_FWD 0
 #endif
 #ifndef VATTN_POLY_DKDV
-#define VATTN_POLY_DKDV 4
+#define VATTN_POLY_DKDV 0
 #endif
 #ifndef VATTN_POLY_DQ
 #define VATTN_POLY_DQ 0
 #endif
+// d = 64: the exponentials per tile are the same as at d = 128 but the MMA work
+// halves, so every kernel is MUFU-bound there and the offload pays.
+#ifndef VATTN_POLY_FWD64
+#define VATTN_POLY_FWD64 4
+#endif
+#ifndef VATTN_POLY_DKDV64
+#define VATTN_POLY_DKDV64 4
+#endif
+#ifndef VATTN_POLY_DQ64
+#define VATTN_POLY_DQ64 0
+#endif
+template <int kD> struct PolyPeriod {
+    static constexpr int fwd = kD == 64 ? VATTN_POLY_FWD64 : VATTN_POLY_FWD;
+    static constexpr int dkdv = kD == 64 ? VATTN_POLY_DKDV64 : VATTN_POLY_DKDV;
+    static constexpr int dq = kD == 64 ? VATTN_POLY_DQ64 : VATTN_POLY_DQ;
+};
 // `pair` is an unrolled loop index, so the branch folds away at compile time.
 template <int kPeriod>
 VATTN_DEV float ex2_mix(int pair, float x) {
