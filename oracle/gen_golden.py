@@ -63,17 +63,51 @@ def make_case(name, shape, causal, tiles, seed, source):
     return dict(name=name, shape=list(shape), causal=causal, tiles=[br, bc], seed=seed, source=source)
 
 
+# dropout cases: name, shape, causal, tiles, input seed, dropout_p, dropout seed, source
+DROP_CASES = [
+    ("drop_p10_n64d32", (1, 1, 64, 32), False, (32, 32), 23, 0.1, 33, "test_forward.cpp:238-253"),
+    ("drop_p10_causal_n64d16", (1, 1, 64, 16), True, (32, 32), 13, 0.1, 77, "test_backward.cpp:129-146"),
+    ("drop_p25_b2h2n128d64", (2, 2, 128, 64), False, (64, 64), 5, 0.25, 1234, "SURVEY 8f-1 (paper grid p)"),
+]
+
+
+def make_drop_case(name, shape, causal, tiles, seed, p, dseed, source):
+    B, H, N, d = shape
+    br, bc = tiles
+    q, k, v, do = (po.ref_normal_f16(seed, s, B * H * N * d).reshape(shape) for s in (1, 2, 3, 4))
+    o32, lse32, dig32 = po.ref_forward_fused_dropout(q, k, v, causal, p, dseed, br, bc, acc_fp16=False)
+    qd, kd, vd, dod = (po.widen(x) for x in (q, k, v, do))
+    o64, lse64 = po.ref_attention_ref_dropout(qd, kd, vd, causal, p, dseed)
+    dq64, dk64, dv64 = po.ref_attention_grad_ref_dropout(qd, kd, vd, dod, causal, p, dseed)
+    o16, lse16, dig16 = po.ref_forward_fused_dropout(q, k, v, causal, p, dseed, br, bc, acc_fp16=True)
+    dq16, dk16, dv16, digb = po.ref_backward_fused_dropout(q, k, v, do, lse16, causal, p, dseed, br, bc)
+    assert dig16 == digb and dig32 == dig16
+    # the keep mask of every position of head (0, 0), as the reference decides it
+    mask = np.array([[po.ref_dropout_keep(dseed, 0, 0, i, j, p) for j in range(N)] for i in range(N)], np.uint8)
+    np.savez_compressed(
+        os.path.join(OUT, name + ".npz"), q=q, k=k, v=v, dout=do, mask_b0h0=mask,
+        fwd32_out=o32, fwd32_lse=lse32, ref_out=o64, ref_lse=lse64, ref_dq=dq64, ref_dk=dk64, ref_dv=dv64,
+        fwd16_lse=lse16, bwd16_dq=dq16, bwd16_dk=dk16, bwd16_dv=dv16, digest=np.uint64(dig32))
+    return dict(name=name, shape=list(shape), causal=causal, tiles=[br, bc], seed=seed, dropout_p=p,
+                dropout_seed=dseed, source=source)
+
+
 def main():
     if not po.ref_available():
         raise SystemExit("oracle/_ref/libvattn_ref.so missing: run `make -C oracle` where /root/reference exists")
     os.makedirs(OUT, exist_ok=True)
     manifest = [make_case(*c) for c in CASES]
+    drop_manifest = [make_drop_case(*c) for c in DROP_CASES]
+    # dropout_keep grid (rng.cpp:46-49) for seed 42, p = 0.5, (b, h) = (0, 1)
+    np.savez_compressed(os.path.join(OUT, "dropout_keep_seed42.npz"),
+                        keep=np.array([[po.ref_dropout_keep(42, 0, 1, i, j, 0.5) for j in range(64)]
+                                       for i in range(64)], np.uint8))
     # Generator pin: the first 256 binary16 normals of (seed 1, stream 1..4).
     np.savez_compressed(os.path.join(OUT, "normals_seed1.npz"),
                         **{f"stream{s}": po.ref_normal_f16(1, s, 256) for s in (1, 2, 3, 4)})
     with open(os.path.join(OUT, "manifest.json"), "w") as f:
         json.dump(dict(generator="oracle/gen_golden.py", reference="/root/reference/proj (vattn, compiled by oracle/Makefile)",
-                       cases=manifest), f, indent=1)
+                       cases=manifest, dropout_cases=drop_manifest), f, indent=1)
     print(f"wrote {len(manifest)} cases to {OUT}")
 
 

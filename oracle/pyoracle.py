@@ -57,6 +57,14 @@ def oracle_lib():
         lib.vo_forward_fused_fp32acc.argtypes = [_i32] * 7 + [_f32, _u16p, _u16p, _u16p, _u16p, _f32p]
         lib.vo_forward_fused_fp32acc.restype = C.c_int
         lib.vo_compute_dpsum.argtypes = [_i32] * 5 + [_u16p, _u16p, _f32p]
+        lib.vo_dropout_keep.argtypes = [_u64] * 5 + [_f32]
+        lib.vo_dropout_keep.restype = C.c_int
+        lib.vo_position_hash.argtypes = [_u64] * 5
+        lib.vo_position_hash.restype = C.c_uint64
+        lib.vo_attention_ref_dropout.argtypes = [_i32] * 5 + [_f32, _f32, _u64] + [_f64p] * 5
+        lib.vo_attention_grad_ref_dropout.argtypes = [_i32] * 5 + [_f32, _f32, _u64] + [_f64p] * 7
+        lib.vo_forward_fused_fp32acc_dropout.argtypes = [_i32] * 7 + [_f32, _f32, _u64, _u16p, _u16p, _u16p, _u16p, _f32p]
+        lib.vo_forward_fused_fp32acc_dropout.restype = C.c_int
         lib.vo_error_metrics.argtypes = [_f64p, _f64p, _u64, _f64p]
         lib.vo_frobenius_rel.argtypes = [_f64p, _f64p, _u64]
         lib.vo_frobenius_rel.restype = C.c_double
@@ -79,6 +87,13 @@ def ref_lib():
         lib.vr_compute_dpsum.argtypes = [_i32] * 4 + [_u16p, _u16p, _f32p]
         lib.vr_attention_ref.argtypes = [_i32] * 5 + [_f32] + [_f64p] * 5
         lib.vr_attention_grad_ref.argtypes = [_i32] * 5 + [_f32] + [_f64p] * 7
+        lib.vr_dropout_keep.argtypes = [_u64] * 5 + [_f32]
+        lib.vr_dropout_keep.restype = C.c_int
+        _u64p = C.POINTER(C.c_uint64)
+        lib.vr_forward_fused_dropout.argtypes = [_i32] * 8 + [_f32, _f32, _u64, _u16p, _u16p, _u16p, _u16p, _f32p, _u64p]
+        lib.vr_backward_fused_dropout.argtypes = [_i32] * 7 + [_f32, _f32, _u64] + [_u16p] * 4 + [_f32p] + [_u16p] * 3 + [_u64p]
+        lib.vr_attention_ref_dropout.argtypes = [_i32] * 5 + [_f32, _f32, _u64] + [_f64p] * 5
+        lib.vr_attention_grad_ref_dropout.argtypes = [_i32] * 5 + [_f32, _f32, _u64] + [_f64p] * 7
         lib.vr_bench_units.argtypes = [_i32] * 5
         lib.vr_bench_units.restype = C.c_double
         _ref = lib
@@ -102,35 +117,43 @@ def widen(bits: np.ndarray, bf16: bool = False) -> np.ndarray:
     return out.reshape(bits.shape)
 
 
-def attention_ref(q, k, v, causal: bool, scale: float = 0.0):
+def attention_ref(q, k, v, causal: bool, scale: float = 0.0, dropout_p: float = 0.0, seed: int = 0):
     """binary64 oracle forward (reference.cpp:26-80) on widened float64 inputs [B,H,N,d]."""
     B, H, N, d = q.shape
     out = np.empty((B, H, N, d), np.float64)
     lse = np.empty((B, H, N), np.float64)
-    oracle_lib().vo_attention_ref(B, H, N, d, int(causal), scale,
-                                  np.ascontiguousarray(q, np.float64), np.ascontiguousarray(k, np.float64),
-                                  np.ascontiguousarray(v, np.float64), out, lse)
+    oracle_lib().vo_attention_ref_dropout(B, H, N, d, int(causal), scale, dropout_p, seed,
+                                          np.ascontiguousarray(q, np.float64), np.ascontiguousarray(k, np.float64),
+                                          np.ascontiguousarray(v, np.float64), out, lse)
     return out, lse
 
 
-def attention_grad_ref(q, k, v, dout, causal: bool, scale: float = 0.0):
+def attention_grad_ref(q, k, v, dout, causal: bool, scale: float = 0.0, dropout_p: float = 0.0, seed: int = 0):
     """binary64 analytic gradients (reference.cpp:82-167)."""
     B, H, N, d = q.shape
     dq = np.empty((B, H, N, d), np.float64)
     dk = np.empty_like(dq)
     dv = np.empty_like(dq)
     c = lambda a: np.ascontiguousarray(a, np.float64)  # noqa: E731
-    oracle_lib().vo_attention_grad_ref(B, H, N, d, int(causal), scale, c(q), c(k), c(v), c(dout), dq, dk, dv)
+    oracle_lib().vo_attention_grad_ref_dropout(B, H, N, d, int(causal), scale, dropout_p, seed,
+                                               c(q), c(k), c(v), c(dout), dq, dk, dv)
     return dq, dk, dv
 
 
-def forward_fused_fp32acc(q16, k16, v16, causal: bool, br: int = 64, bc: int = 64, scale: float = 0.0):
+def dropout_keep(seed, b, h, row, col, p) -> bool:
+    """rng.cpp:46-49."""
+    return bool(oracle_lib().vo_dropout_keep(seed, b, h, row, col, p))
+
+
+def forward_fused_fp32acc(q16, k16, v16, causal: bool, br: int = 64, bc: int = 64, scale: float = 0.0,
+                          dropout_p: float = 0.0, seed: int = 0):
     """Bit-exact restatement of forward_fused at FP32-ACC (attention_forward.cpp:110-227)."""
     B, H, N, d = q16.shape
     out = np.empty((B, H, N, d), np.uint16)
     lse = np.empty((B, H, N), np.float32)
     c = lambda a: np.ascontiguousarray(a, np.uint16)  # noqa: E731
-    rc = oracle_lib().vo_forward_fused_fp32acc(B, H, N, d, br, bc, int(causal), scale, c(q16), c(k16), c(v16), out, lse)
+    rc = oracle_lib().vo_forward_fused_fp32acc_dropout(B, H, N, d, br, bc, int(causal), scale, dropout_p, seed,
+                                                       c(q16), c(k16), c(v16), out, lse)
     if rc == -1:
         raise ValueError("forward_fused: invalid config")
     if rc == -2:
@@ -229,3 +252,58 @@ def ref_compute_dpsum(dout16, o16):
 def ref_bench_units(N: int, d: int, causal: bool, units: int, threads: int) -> float:
     """Seconds for `units` x (forward_fused FP32-ACC + backward_fused) on `threads` host threads."""
     return float(ref_lib().vr_bench_units(N, d, int(causal), units, threads))
+
+
+def ref_dropout_keep(seed, b, h, row, col, p) -> bool:
+    return bool(ref_lib().vr_dropout_keep(seed, b, h, row, col, p))
+
+
+def ref_forward_fused_dropout(q16, k16, v16, causal, dropout_p, seed, br=64, bc=64, acc_fp16=False, scale=0.0):
+    B, H, N, d = q16.shape
+    out = np.empty((B, H, N, d), np.uint16)
+    lse = np.empty((B, H, N), np.float32)
+    dig = C.c_uint64(0)
+    c = lambda a: np.ascontiguousarray(a, np.uint16)  # noqa: E731
+    lib = ref_lib()
+    rc = lib.vr_forward_fused_dropout(B, H, N, d, br, bc, int(causal), int(acc_fp16), scale, dropout_p, seed,
+                                      c(q16), c(k16), c(v16), out, lse, C.byref(dig))
+    if rc:
+        raise RuntimeError(lib.vr_last_error().decode())
+    return out, lse, dig.value
+
+
+def ref_backward_fused_dropout(q16, k16, v16, dout16, lse, causal, dropout_p, seed, br=64, bc=64, scale=0.0):
+    B, H, N, d = q16.shape
+    dq = np.empty((B, H, N, d), np.uint16)
+    dk = np.empty_like(dq)
+    dv = np.empty_like(dq)
+    dig = C.c_uint64(0)
+    c = lambda a: np.ascontiguousarray(a, np.uint16)  # noqa: E731
+    lib = ref_lib()
+    rc = lib.vr_backward_fused_dropout(B, H, N, d, br, bc, int(causal), scale, dropout_p, seed, c(q16), c(k16),
+                                       c(v16), c(dout16), np.ascontiguousarray(lse, np.float32), dq, dk, dv,
+                                       C.byref(dig))
+    if rc:
+        raise RuntimeError(lib.vr_last_error().decode())
+    return dq, dk, dv, dig.value
+
+
+def ref_attention_ref_dropout(q, k, v, causal, dropout_p, seed, scale=0.0):
+    B, H, N, d = q.shape
+    out = np.empty((B, H, N, d), np.float64)
+    lse = np.empty((B, H, N), np.float64)
+    c = lambda a: np.ascontiguousarray(a, np.float64)  # noqa: E731
+    assert ref_lib().vr_attention_ref_dropout(B, H, N, d, int(causal), scale, dropout_p, seed, c(q), c(k), c(v),
+                                              out, lse) == 0
+    return out, lse
+
+
+def ref_attention_grad_ref_dropout(q, k, v, dout, causal, dropout_p, seed, scale=0.0):
+    B, H, N, d = q.shape
+    dq = np.empty((B, H, N, d), np.float64)
+    dk = np.empty_like(dq)
+    dv = np.empty_like(dq)
+    c = lambda a: np.ascontiguousarray(a, np.float64)  # noqa: E731
+    assert ref_lib().vr_attention_grad_ref_dropout(B, H, N, d, int(causal), scale, dropout_p, seed, c(q), c(k),
+                                                   c(v), c(dout), dq, dk, dv) == 0
+    return dq, dk, dv

@@ -14,6 +14,8 @@
 //   vr_attention_ref      -> vattn::attention_ref       include/vattn/reference.hpp:22-23
 //   vr_attention_grad_ref -> vattn::attention_grad_ref  include/vattn/reference.hpp:31-34
 //   vr_normal_tensor_f16  -> vattn::normal_tensor_f16   include/vattn/workload.hpp:10-17
+//   vr_*_dropout          -> the same entry points with AttnConfig::dropout_p / seed set
+//   vr_dropout_keep       -> vattn::dropout_keep                include/vattn/rng.hpp:22-26
 //   vr_bench_units        -> forward_fused + backward_fused over (b,h) units on host threads
 #include <atomic>
 #include <chrono>
@@ -54,7 +56,7 @@ Tensor<double> from_f64(const double* p, int B, int H, int N, int d) {
 }
 
 AttnConfig make_cfg(int B, int H, int N, int d, int br, int bc, int causal, int acc_fp16,
-                    float scale) {
+                    float scale, float dropout_p = 0.0f, uint64_t seed = 0) {
     AttnConfig c;
     c.batch = B;
     c.heads = H;
@@ -65,6 +67,8 @@ AttnConfig make_cfg(int B, int H, int N, int d, int br, int bc, int causal, int 
     c.causal = causal != 0;
     c.acc_mode = acc_fp16 ? AccMode::FP16_ACC : AccMode::FP32_ACC;
     c.softmax_scale = scale;
+    c.dropout_p = dropout_p;
+    c.seed = seed;
     return c;
 }
 
@@ -154,6 +158,75 @@ int vr_attention_grad_ref(int B, int H, int N, int d, int causal, float scale, c
                           double* dk, double* dv) {
     return guarded([&] {
         const AttnConfig cfg = make_cfg(B, H, N, d, 8, 8, causal, 0, scale);
+        const RefGrads g =
+            attention_grad_ref(from_f64(q, B, H, N, d), from_f64(k, B, H, N, d),
+                               from_f64(v, B, H, N, d), from_f64(dout, B, H, N, d), cfg);
+        std::memcpy(dq, g.dq.data(), g.dq.size() * sizeof(double));
+        std::memcpy(dk, g.dk.data(), g.dk.size() * sizeof(double));
+        std::memcpy(dv, g.dv.data(), g.dv.size() * sizeof(double));
+    });
+}
+
+// Dropout variants (rng.cpp:35-54; attention_forward.cpp:77-106; attention_backward.cpp:145-160;
+// reference.cpp:66-69, 118-121).  mask_digest is returned for completeness.
+int vr_dropout_keep(uint64_t seed, uint64_t b, uint64_t h, uint64_t row, uint64_t col, float p) {
+    return dropout_keep(seed, b, h, row, col, p) ? 1 : 0;
+}
+
+int vr_forward_fused_dropout(int B, int H, int N, int d, int br, int bc, int causal, int acc_fp16,
+                             float scale, float dropout_p, uint64_t seed, const uint16_t* q,
+                             const uint16_t* k, const uint16_t* v, uint16_t* out, float* lse,
+                             uint64_t* digest) {
+    return guarded([&] {
+        const AttnConfig cfg = make_cfg(B, H, N, d, br, bc, causal, acc_fp16, scale, dropout_p, seed);
+        const ForwardOutput r = forward_fused(from_bits(q, B, H, N, d), from_bits(k, B, H, N, d),
+                                              from_bits(v, B, H, N, d), cfg);
+        for (std::size_t i = 0; i < r.out.size(); ++i) out[i] = r.out.data()[i].bits;
+        std::memcpy(lse, r.lse.data(), r.lse.size() * sizeof(float));
+        *digest = r.mask_digest;
+    });
+}
+
+int vr_backward_fused_dropout(int B, int H, int N, int d, int br, int bc, int causal, float scale,
+                              float dropout_p, uint64_t seed, const uint16_t* q, const uint16_t* k,
+                              const uint16_t* v, const uint16_t* dout, const float* lse,
+                              uint16_t* dq, uint16_t* dk, uint16_t* dv, uint64_t* digest) {
+    return guarded([&] {
+        const AttnConfig cfg = make_cfg(B, H, N, d, br, bc, causal, 1, scale, dropout_p, seed);
+        Tensor<float> l(std::vector<std::size_t>{static_cast<std::size_t>(B),
+                                                 static_cast<std::size_t>(H),
+                                                 static_cast<std::size_t>(N)});
+        std::memcpy(l.data(), lse, l.size() * sizeof(float));
+        const GradOutputs g =
+            backward_fused(from_bits(q, B, H, N, d), from_bits(k, B, H, N, d),
+                           from_bits(v, B, H, N, d), from_bits(dout, B, H, N, d), l, cfg);
+        for (std::size_t i = 0; i < g.dq.size(); ++i) {
+            dq[i] = g.dq.data()[i].bits;
+            dk[i] = g.dk.data()[i].bits;
+            dv[i] = g.dv.data()[i].bits;
+        }
+        *digest = g.mask_digest;
+    });
+}
+
+int vr_attention_ref_dropout(int B, int H, int N, int d, int causal, float scale, float dropout_p,
+                             uint64_t seed, const double* q, const double* k, const double* v,
+                             double* out, double* lse) {
+    return guarded([&] {
+        const AttnConfig cfg = make_cfg(B, H, N, d, 8, 8, causal, 0, scale, dropout_p, seed);
+        const RefForward r = attention_ref(from_f64(q, B, H, N, d), from_f64(k, B, H, N, d),
+                                           from_f64(v, B, H, N, d), cfg);
+        std::memcpy(out, r.out.data(), r.out.size() * sizeof(double));
+        std::memcpy(lse, r.lse.data(), r.lse.size() * sizeof(double));
+    });
+}
+
+int vr_attention_grad_ref_dropout(int B, int H, int N, int d, int causal, float scale,
+                                  float dropout_p, uint64_t seed, const double* q, const double* k,
+                                  const double* v, const double* dout, double* dq, double* dk,
+                                  double* dv) {
+    return guarded([&] {
+        const AttnConfig cfg = make_cfg(B, H, N, d, 8, 8, causal, 0, scale, dropout_p, seed);
         const RefGrads g =
             attention_grad_ref(from_f64(q, B, H, N, d), from_f64(k, B, H, N, d),
                                from_f64(v, B, H, N, d), from_f64(dout, B, H, N, d), cfg);

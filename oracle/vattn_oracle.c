@@ -17,12 +17,13 @@
  *   vo_f32_to_f16 / vo_f16_to_f32            src/half.cpp:5-65 (bit-exact)
  *   vo_f32_to_bf16 / vo_bf16_to_f32          RNE bf16 (no reference counterpart)
  *   vo_normal_tensor_f16                     include/vattn/workload.hpp:10-17 (bit-exact)
- *   vo_attention_ref                         src/reference.cpp:26-80 (bit-exact, p = 0)
- *   vo_attention_grad_ref                    src/reference.cpp:82-167 (bit-exact, p = 0)
- *   vo_forward_fused_fp32acc                 src/attention_forward.cpp:110-227 with the
- *        FP32-ACC dot4 contract of src/half.cpp:67-77 and the tile loop order of
- *        src/tile_pipeline.cpp:33-49; online softmax src/online_softmax.cpp:21-87
- *        (bit-exact for dropout_p = 0)
+ *   vo_position_hash / vo_dropout_keep       src/rng.cpp:35-49 (bit-exact)
+ *   vo_attention_ref[_dropout]               src/reference.cpp:26-80 (bit-exact)
+ *   vo_attention_grad_ref[_dropout]          src/reference.cpp:82-167 (bit-exact)
+ *   vo_forward_fused_fp32acc[_dropout]       src/attention_forward.cpp:110-227 with the
+ *        FP32-ACC dot4 contract of src/half.cpp:67-77, the tile loop order of
+ *        src/tile_pipeline.cpp:33-49, online softmax src/online_softmax.cpp:21-87
+ *        and apply_dropout (:77-106) (bit-exact)
  *   vo_compute_dpsum                         src/attention_backward.cpp:44-57 (bit-exact)
  *   vo_error_metrics / vo_frobenius_rel      src/reference.cpp:186-222
  *
@@ -61,6 +62,21 @@ VO_EXPORT float vo_normal_at(uint64_t seed, uint64_t index) {
     const double u1 = 1.0 - vo_bits_to_unit(a);
     const double u2 = vo_bits_to_unit(b);
     return (float)(sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793238462643383279502884 * u2));
+}
+
+/* src/rng.cpp:35-42 position hash and :46-49 dropout_keep (keep iff u >= p). */
+VO_EXPORT uint64_t vo_position_hash(uint64_t seed, uint64_t b, uint64_t h, uint64_t row, uint64_t col) {
+    uint64_t s = vo_hash_combine(seed, 0x64726f70ull); /* "drop" stream tag */
+    s = vo_hash_combine(s, b);
+    s = vo_hash_combine(s, h);
+    s = vo_hash_combine(s, row);
+    s = vo_hash_combine(s, col);
+    return s;
+}
+
+VO_EXPORT int vo_dropout_keep(uint64_t seed, uint64_t b, uint64_t h, uint64_t row, uint64_t col, float p) {
+    if (p <= 0.0f) return 1;
+    return vo_bits_to_unit(vo_position_hash(seed, b, h, row, col)) >= (double)p;
 }
 
 /* ------------------------------------------------------------- binary16 -- */
@@ -152,10 +168,22 @@ static double cfg_scale(float scale, int d) {
     return scale > 0.0f ? (double)scale : (double)(1.0f / sqrtf((float)d));
 }
 
+VO_EXPORT void vo_attention_ref_dropout(int B, int H, int N, int d, int causal, float scale_f,
+                                        float p_drop, uint64_t seed, const double* q, const double* k,
+                                        const double* v, double* out, double* lse);
+
 VO_EXPORT void vo_attention_ref(int B, int H, int N, int d, int causal, float scale_f,
                                 const double* q, const double* k, const double* v,
                                 double* out, double* lse) {
+    vo_attention_ref_dropout(B, H, N, d, causal, scale_f, 0.0f, 0, q, k, v, out, lse);
+}
+
+/* src/reference.cpp:26-80 including the dropout branch (:66-69). */
+VO_EXPORT void vo_attention_ref_dropout(int B, int H, int N, int d, int causal, float scale_f,
+                                        float p_drop, uint64_t seed, const double* q, const double* k,
+                                        const double* v, double* out, double* lse) {
     const double scale = cfg_scale(scale_f, d);
+    const double inv_keep = 1.0 / (1.0 - (double)p_drop);
     double* s = (double*)malloc(sizeof(double) * (size_t)N);
     double* p = (double*)malloc(sizeof(double) * (size_t)N);
     for (int bh = 0; bh < B * H; ++bh) {
@@ -177,7 +205,12 @@ VO_EXPORT void vo_attention_ref(int B, int H, int N, int d, int causal, float sc
             double l = 0.0;
             for (int j = 0; j < N; ++j) l += s[j] == -INFINITY ? 0.0 : exp(s[j] - m);
             lse[(size_t)bh * N + i] = m + log(l);
-            for (int j = 0; j < N; ++j) p[j] = s[j] == -INFINITY ? 0.0 : exp(s[j] - m) / l;
+            for (int j = 0; j < N; ++j) {
+                p[j] = s[j] == -INFINITY ? 0.0 : exp(s[j] - m) / l;
+                if (p_drop > 0.0f)
+                    p[j] = vo_dropout_keep(seed, (uint64_t)(bh / H), (uint64_t)(bh % H), (uint64_t)i, (uint64_t)j, p_drop)
+                               ? p[j] * inv_keep : 0.0;
+            }
             for (int e = 0; e < d; ++e) {
                 double acc = 0.0;
                 for (int j = 0; j < N; ++j) acc += p[j] * V[(size_t)j * d + e];
@@ -192,10 +225,25 @@ VO_EXPORT void vo_attention_ref(int B, int H, int N, int d, int causal, float sc
 /* src/reference.cpp:82-167 (dropout_p = 0): analytic gradients in binary64.
  *   dV = P^T dO, dP = dO V^T, dS = P o (dP - rowsum(dP o P)) * scale,
  *   dQ = dS K, dK = dS^T Q. */
+VO_EXPORT void vo_attention_grad_ref_dropout(int B, int H, int N, int d, int causal, float scale_f,
+                                             float p_drop, uint64_t seed, const double* q, const double* k,
+                                             const double* v, const double* dout, double* dq, double* dk,
+                                             double* dv);
+
 VO_EXPORT void vo_attention_grad_ref(int B, int H, int N, int d, int causal, float scale_f,
                                      const double* q, const double* k, const double* v,
                                      const double* dout, double* dq, double* dk, double* dv) {
+    vo_attention_grad_ref_dropout(B, H, N, d, causal, scale_f, 0.0f, 0, q, k, v, dout, dq, dk, dv);
+}
+
+/* src/reference.cpp:82-167 including the dropout factor matrix D (:118-121). */
+VO_EXPORT void vo_attention_grad_ref_dropout(int B, int H, int N, int d, int causal, float scale_f,
+                                             float p_drop, uint64_t seed, const double* q, const double* k,
+                                             const double* v, const double* dout, double* dq, double* dk,
+                                             double* dv) {
     const double scale = cfg_scale(scale_f, d);
+    const double inv_keep = 1.0 / (1.0 - (double)p_drop);
+    double* drop = (double*)malloc(sizeof(double) * (size_t)N * N);
     const size_t nn = (size_t)N * N;
     double* p = (double*)malloc(sizeof(double) * nn);
     double* dp = (double*)malloc(sizeof(double) * nn);
@@ -218,19 +266,25 @@ VO_EXPORT void vo_attention_grad_ref(int B, int H, int N, int d, int causal, flo
             }
             double l = 0.0;
             for (int j = 0; j < N; ++j) l += s[j] == -INFINITY ? 0.0 : exp(s[j] - m);
-            for (int j = 0; j < N; ++j) p[(size_t)i * N + j] = s[j] == -INFINITY ? 0.0 : exp(s[j] - m) / l;
+            for (int j = 0; j < N; ++j) {
+                p[(size_t)i * N + j] = s[j] == -INFINITY ? 0.0 : exp(s[j] - m) / l;
+                drop[(size_t)i * N + j] =
+                    p_drop > 0.0f ? (vo_dropout_keep(seed, (uint64_t)(bh / H), (uint64_t)(bh % H), (uint64_t)i,
+                                                     (uint64_t)j, p_drop) ? inv_keep : 0.0)
+                                  : 1.0;
+            }
         }
         for (int j = 0; j < N; ++j)
             for (int e = 0; e < d; ++e) {
                 double acc = 0.0;
-                for (int i = 0; i < N; ++i) acc += 1.0 * p[(size_t)i * N + j] * DO[(size_t)i * d + e];
+                for (int i = 0; i < N; ++i) acc += drop[(size_t)i * N + j] * p[(size_t)i * N + j] * DO[(size_t)i * d + e];
                 dv[off + (size_t)j * d + e] = acc;
             }
         for (int i = 0; i < N; ++i) {
             for (int j = 0; j < N; ++j) {
                 double acc = 0.0;
                 for (int e = 0; e < d; ++e) acc += DO[(size_t)i * d + e] * V[(size_t)j * d + e];
-                dp[(size_t)i * N + j] = 1.0 * acc;
+                dp[(size_t)i * N + j] = drop[(size_t)i * N + j] * acc;
             }
             double dpsum = 0.0;
             for (int j = 0; j < N; ++j) dpsum += dp[(size_t)i * N + j] * p[(size_t)i * N + j];
@@ -254,6 +308,7 @@ VO_EXPORT void vo_attention_grad_ref(int B, int H, int N, int d, int causal, flo
     free(dp);
     free(ds);
     free(s);
+    free(drop);
 }
 
 /* ------------------------------------------- fused FP32-ACC forward ---- */
@@ -277,9 +332,23 @@ static inline float dot_fp32acc(float acc, const float* a, const float* b, int b
  * Returns 0, or -1 for a config AttnConfig::validate() rejects
  * (src/attention_forward.cpp:31-40), or -2 for a fully masked row
  * (src/online_softmax.cpp:81-82). */
+VO_EXPORT int vo_forward_fused_fp32acc_dropout(int B, int H, int N, int d, int br, int bc, int causal,
+                                               float scale_f, float p_drop, uint64_t seed, const uint16_t* q,
+                                               const uint16_t* k, const uint16_t* v, uint16_t* out, float* lse);
+
 VO_EXPORT int vo_forward_fused_fp32acc(int B, int H, int N, int d, int br, int bc, int causal,
                                        float scale_f, const uint16_t* q, const uint16_t* k,
                                        const uint16_t* v, uint16_t* out, float* lse) {
+    return vo_forward_fused_fp32acc_dropout(B, H, N, d, br, bc, causal, scale_f, 0.0f, 0, q, k, v, out, lse);
+}
+
+/* ... with the dropout step of src/attention_forward.cpp:77-106 (applied to the
+ * binary16 P fragments: kept weights f16(f16(P) * (1/(1-p))), dropped ones 0). */
+VO_EXPORT int vo_forward_fused_fp32acc_dropout(int B, int H, int N, int d, int br, int bc, int causal,
+                                               float scale_f, float p_drop, uint64_t seed, const uint16_t* q,
+                                               const uint16_t* k, const uint16_t* v, uint16_t* out, float* lse) {
+    if (!(p_drop >= 0.0f && p_drop < 1.0f)) return -1;
+    const float inv_keep = 1.0f / (1.0f - p_drop);
     if (B < 1 || H < 1 || N <= 0 || d <= 0 || br <= 0 || br % 8 || bc <= 0 || bc % 8 || d % 4 ||
         N % br || N % bc)
         return -1;
@@ -337,7 +406,13 @@ VO_EXPORT int vo_forward_fused_fp32acc(int B, int H, int N, int d, int br, int b
                         const float x = s[(size_t)i * bc + j];
                         const float w = x == -INFINITY ? 0.0f : expf(x - m_new);
                         bsum += w;
-                        p16[(size_t)i * bc + j] = vo_f16_to_f32(vo_f32_to_f16(w)); /* :163-167 */
+                        float pw = vo_f16_to_f32(vo_f32_to_f16(w)); /* :163-167 */
+                        if (p_drop > 0.0f)
+                            pw = vo_dropout_keep(seed, (uint64_t)(bh / H), (uint64_t)(bh % H), (uint64_t)(row0 + i),
+                                                 (uint64_t)(col0 + j), p_drop)
+                                     ? vo_f16_to_f32(vo_f32_to_f16(pw * inv_keep))
+                                     : 0.0f;
+                        p16[(size_t)i * bc + j] = pw;
                     }
                     l[i] = l[i] * resc + bsum;
                     m[i] = m_new;

@@ -120,3 +120,39 @@ def test_restatement_matches_live_reference_random_config():
         a = po.forward_fused_fp32acc(q, k, v, causal, 32, 48)
         b = po.ref_forward_fused(q, k, v, causal, 32, 48)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+
+
+# ---------------------------------------------------------------- dropout --
+DROP = json.load(open(os.path.join(GOLDEN, "manifest.json")))["dropout_cases"]
+
+
+def test_dropout_keep_matches_reference_grid():
+    """rng.cpp:46-49 restated bit-exactly (seed 42, p 0.5, b 0, h 1)."""
+    g = load("dropout_keep_seed42")["keep"]
+    ours = np.array([[po.dropout_keep(42, 0, 1, i, j, 0.5) for j in range(64)] for i in range(64)], np.uint8)
+    assert np.array_equal(ours, g)
+    assert po.dropout_keep(42, 0, 1, 2, 3, 0.0)  # p = 0 short-circuit (test_forward.cpp:227)
+
+
+def test_dropout_keep_rate():
+    """acceptance criterion 9: keep rate 0.9 +/- 0.002 at p = 0.1 (sampled)."""
+    kept = sum(po.dropout_keep(42, 0, 0, i // 300, i % 300, 0.1) for i in range(90000))
+    assert abs(kept / 90000 - 0.9) <= 0.004
+
+
+@pytest.mark.parametrize("case", DROP, ids=[c["name"] for c in DROP])
+def test_dropout_restatements_bitexact(case):
+    g = load(case["name"])
+    p, ds = case["dropout_p"], case["dropout_seed"]
+    br, bc = case["tiles"]
+    N = case["shape"][2]
+    mask = np.array([[po.dropout_keep(ds, 0, 0, i, j, p) for j in range(N)] for i in range(N)], np.uint8)
+    assert np.array_equal(mask, g["mask_b0h0"])
+    out, lse = po.forward_fused_fp32acc(g["q"], g["k"], g["v"], case["causal"], br, bc, dropout_p=p, seed=ds)
+    assert np.array_equal(out, g["fwd32_out"])
+    assert np.array_equal(lse.view(np.uint32), g["fwd32_lse"].view(np.uint32))
+    q, k, v, do = (po.widen(g[x]) for x in ("q", "k", "v", "dout"))
+    o, l = po.attention_ref(q, k, v, case["causal"], dropout_p=p, seed=ds)
+    assert np.array_equal(o, g["ref_out"]) and np.array_equal(l, g["ref_lse"])
+    dq, dk, dv = po.attention_grad_ref(q, k, v, do, case["causal"], dropout_p=p, seed=ds)
+    assert np.array_equal(dq, g["ref_dq"]) and np.array_equal(dk, g["ref_dk"]) and np.array_equal(dv, g["ref_dv"])
