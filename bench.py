@@ -184,6 +184,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--dropout", type=float, default=0.0, help="fused dropout p (reference keep masks); 0 = north_star")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -212,8 +213,9 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        vb.mha_forward(q, k, v, causal, out=o, lse=lse)
-        vb.mha_backward(q, k, v, o, do, lse, causal, dq=dq, dk=dk, dv=dv, workspace=ws)
+        vb.mha_forward(q, k, v, causal, out=o, lse=lse, dropout_p=args.dropout, seed=1234)
+        vb.mha_backward(q, k, v, o, do, lse, causal, dq=dq, dk=dk, dv=dv, workspace=ws,
+                        dropout_p=args.dropout, seed=1234)
 
     for _ in range(args.warmup):
         step()
@@ -307,7 +309,8 @@ def main():
             "config": {"workload": desc, "batch_per_gpu": B, "heads": H, "seq_len": N, "head_dim": d,
                        "causal": causal, "global_batch": B * world, "parallelism": f"(batch,head) shards x{world}, no collective",
                        "l2": "inputs (4 x %d MiB) exceed the 126 MB L2; no flush" % (q.numel() * 2 >> 20),
-                       "flop_model": "fwd 4BHN^2d*c + bwd 10BHN^2d*c, c=1/2 causal"},
+                       "flop_model": "fwd 4BHN^2d*c + bwd 10BHN^2d*c, c=1/2 causal",
+                       "dropout_p": args.dropout},
             "pct_of_peak": value / world / peak_sust,
             "kernels_ms": {"fwd": fwd_ms, "bwd_dkdv": dkdv_ms, "bwd_dq": dq_ms,
                            "bwd_other(preprocess)": ms_step - fwd_ms - dkdv_ms - dq_ms},

@@ -26,6 +26,12 @@
  *     include/vattn_b200/mha.hpp zero-pads other head dims); any seq_len >= 1.
  *   - No CPU fallback: when the sm_100a kernels cannot run, calls fail with
  *     VATTN_ECUDA / VATTN_EUNSUPPORTED.
+ *   - Dropout (dropout_p > 0) follows the reference exactly: the same stateless
+ *     SplitMix64 position hash decides every keep bit (proj/src/rng.cpp:35-49),
+ *     the forward scales the 16-bit P by 1/(1-p) after its first rounding
+ *     (attention_forward.cpp:77-106) and the backward replays the mask
+ *     (attention_backward.cpp:145-182).  The reference's mask_digest is a
+ *     tiling-dependent test hook and is not produced.
  *
  * Divergence from the reference (documented): the backward takes O as an
  * input (D = rowsum(dO o O) is computed from it) instead of re-running the
@@ -42,7 +48,7 @@
 extern "C" {
 #endif
 
-#define VATTN_B200_ABI_VERSION 1
+#define VATTN_B200_ABI_VERSION 2
 
 typedef enum vattn_status {
     VATTN_OK = 0,
@@ -62,6 +68,9 @@ typedef struct vattn_config {
     int32_t causal;         /* top-left causal mask: key j visible iff j <= i      */
     float softmax_scale;    /* <= 0 selects 1/sqrt(head_dim) (AttnConfig::scale)   */
     int32_t dtype;          /* vattn_dtype                                         */
+    float dropout_p;        /* in [0, 1); 0 = no dropout (AttnConfig::dropout_p)   */
+    uint64_t seed;          /* dropout seed: keep masks are bit-identical to the
+                               reference's dropout_keep(seed, b, h, row, col, p)   */
 } vattn_config;
 
 /* O = softmax(Q K^T * scale [+ causal mask]) V ;  lse = logsumexp per query row. */

@@ -134,6 +134,8 @@ inline vattn_config to_c(const AttnConfig& c, int dn) {
     r.causal = c.causal ? 1 : 0;
     r.softmax_scale = c.scale();  // scale of the true head_dim, not the padded one
     r.dtype = c.dtype;
+    r.dropout_p = c.dropout_p;
+    r.seed = c.seed;
     return r;
 }
 
@@ -146,7 +148,6 @@ inline void forward_fused_device(const AttnConfig& cfg, const void* q, const voi
     cfg.validate();
     if (cfg.head_dim != 64 && cfg.head_dim != 128)
         throw std::invalid_argument("forward_fused_device: head_dim must be 64 or 128 (use the host overload to pad)");
-    if (cfg.dropout_p > 0.0f) throw std::invalid_argument("dropout is not on the B200 path");
     const vattn_config c = detail::to_c(cfg, cfg.head_dim);
     detail::check(mha_forward(&c, q, k, v, out, lse, stream), "mha_forward");
 }
@@ -158,7 +159,6 @@ inline void backward_fused_device(const AttnConfig& cfg, const void* q, const vo
     cfg.validate();
     if (cfg.head_dim != 64 && cfg.head_dim != 128)
         throw std::invalid_argument("backward_fused_device: head_dim must be 64 or 128");
-    if (cfg.dropout_p > 0.0f) throw std::invalid_argument("dropout is not on the B200 path");
     const vattn_config c = detail::to_c(cfg, cfg.head_dim);
     detail::check(mha_backward(&c, q, k, v, out, d_out, lse, dq, dk, dv, workspace, workspace_bytes, stream),
                   "mha_backward");
@@ -170,7 +170,6 @@ inline void backward_fused_device(const AttnConfig& cfg, const void* q, const vo
 inline ForwardOutput forward_fused(const std::vector<uint16_t>& q, const std::vector<uint16_t>& k,
                                    const std::vector<uint16_t>& v, const AttnConfig& cfg) {
     cfg.validate();
-    if (cfg.dropout_p > 0.0f) throw std::invalid_argument("dropout is not on the B200 path");
     if (q.size() != cfg.elems() || k.size() != cfg.elems() || v.size() != cfg.elems())
         throw std::invalid_argument("forward_fused: Q/K/V shape mismatch");
     const int dn = detail::native_dim(cfg.head_dim);
@@ -198,7 +197,6 @@ inline GradOutputs backward_fused(const std::vector<uint16_t>& q, const std::vec
                                   const std::vector<uint16_t>& v, const std::vector<uint16_t>& d_out,
                                   const std::vector<float>& lse, const AttnConfig& cfg) {
     cfg.validate();
-    if (cfg.dropout_p > 0.0f) throw std::invalid_argument("dropout is not on the B200 path");
     if (q.size() != cfg.elems() || k.size() != cfg.elems() || v.size() != cfg.elems() ||
         d_out.size() != cfg.elems())
         throw std::invalid_argument("backward_fused: input shape mismatch");

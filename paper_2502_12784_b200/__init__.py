@@ -44,6 +44,7 @@ class _Cfg(C.Structure):
     _fields_ = [
         ("batch", C.c_int32), ("heads", C.c_int32), ("seq_len", C.c_int32), ("head_dim", C.c_int32),
         ("causal", C.c_int32), ("softmax_scale", C.c_float), ("dtype", C.c_int32),
+        ("dropout_p", C.c_float), ("seed", C.c_uint64),
     ]
 
 
@@ -126,9 +127,9 @@ def _dtype_code(t: torch.Tensor) -> int:
     raise ValueError(f"tensors must be float16 or bfloat16, got {t.dtype}")
 
 
-def _cfg(q: torch.Tensor, causal: bool, softmax_scale: float) -> _Cfg:
+def _cfg(q: torch.Tensor, causal: bool, softmax_scale: float, dropout_p: float = 0.0, seed: int = 0) -> _Cfg:
     B, H, N, d = q.shape
-    return _Cfg(B, H, N, d, 1 if causal else 0, float(softmax_scale), _dtype_code(q))
+    return _Cfg(B, H, N, d, 1 if causal else 0, float(softmax_scale), _dtype_code(q), float(dropout_p), int(seed))
 
 
 def _check(ts, shape, dtype, names):
@@ -159,14 +160,16 @@ def _pad(t: torch.Tensor, dn: int) -> torch.Tensor:
     return t if t.shape[-1] == dn else torch.nn.functional.pad(t, (0, dn - t.shape[-1])).contiguous()
 
 
-def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=None, lse=None):
+def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=None, lse=None,
+                dropout_p: float = 0.0, seed: int = 0):
     """C ABI ``mha_forward`` on CUDA tensors [B, H, N, d] (d in {64, 128}).
-    Returns (out, lse) with lse [B, H, N] fp32 natural-log."""
+    Returns (out, lse) with lse [B, H, N] fp32 natural-log.  ``dropout_p > 0``
+    applies the reference's dropout (keep bits = vattn::dropout_keep(seed, b, h, row, col, p))."""
     _check((q, k, v), q.shape, q.dtype, ("q", "k", "v"))
     B, H, N, d = q.shape
     out = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
-    cfg = _cfg(q, causal, softmax_scale)
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
     rc = lib.mha_forward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                          lse.data_ptr(), _stream())
     if rc:
@@ -175,18 +178,18 @@ def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=N
 
 
 def workspace_bytes(B, H, N, d, causal=False, dtype=torch.float16) -> int:
-    cfg = _Cfg(B, H, N, d, 1 if causal else 0, 0.0, VATTN_BF16 if dtype == torch.bfloat16 else VATTN_F16)
+    cfg = _Cfg(B, H, N, d, 1 if causal else 0, 0.0, VATTN_BF16 if dtype == torch.bfloat16 else VATTN_F16, 0.0, 0)
     return int(lib.mha_backward_workspace_bytes(C.byref(cfg)))
 
 
 def mha_backward(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: float = 0.0,
-                 dq=None, dk=None, dv=None, workspace=None):
+                 dq=None, dk=None, dv=None, workspace=None, dropout_p: float = 0.0, seed: int = 0):
     """C ABI ``mha_backward`` on CUDA tensors.  Returns (dq, dk, dv)."""
     _check((q, k, v, o, dout), q.shape, q.dtype, ("q", "k", "v", "o", "dout"))
     B, H, N, d = q.shape
     if lse.shape != (B, H, N) or lse.dtype != torch.float32 or not lse.is_contiguous():
         raise ValueError("lse must be a contiguous float32 [B, H, N] tensor")
-    cfg = _cfg(q, causal, softmax_scale)
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
     need = int(lib.mha_backward_workspace_bytes(C.byref(cfg)))
     if need == 0:
         rc = lib.mha_backward(C.byref(cfg), *([None] * 10), 0, None)
@@ -208,8 +211,6 @@ def mha_backward(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: flo
 
 def _prep(cfg: AttnConfig, *ts):
     cfg.validate(strict_tiles=False)
-    if cfg.dropout_p > 0.0:
-        raise NotImplementedError("dropout is not on this path (BASELINE north_star runs p = 0)")
     shape = (cfg.batch, cfg.heads, cfg.seq_len, cfg.head_dim)
     for t in ts:
         if tuple(t.shape) != shape:
@@ -222,7 +223,7 @@ def forward_fused(q, k, v, cfg: AttnConfig):
     """vattn::forward_fused on CUDA tensors: returns (out, lse).  head_dim other
     than 64/128 is zero-padded (exact: padded columns add 0 to every dot product)."""
     (qp, kp, vp), dn = _prep(cfg, q, k, v)
-    out, lse = mha_forward(qp, kp, vp, cfg.causal, cfg.scale())
+    out, lse = mha_forward(qp, kp, vp, cfg.causal, cfg.scale(), dropout_p=cfg.dropout_p, seed=cfg.seed)
     return out[..., : cfg.head_dim].contiguous(), lse
 
 
@@ -232,10 +233,11 @@ def backward_fused(q, k, v, d_out, lse, cfg: AttnConfig, out=None):
     when ``out`` is not given."""
     (qp, kp, vp, dop), dn = _prep(cfg, q, k, v, d_out)
     if out is None:
-        op, _ = mha_forward(qp, kp, vp, cfg.causal, cfg.scale())
+        op, _ = mha_forward(qp, kp, vp, cfg.causal, cfg.scale(), dropout_p=cfg.dropout_p, seed=cfg.seed)
     else:
         op = _pad(out.contiguous(), dn)
-    dq, dk, dv = mha_backward(qp, kp, vp, op, dop, lse.contiguous(), cfg.causal, cfg.scale())
+    dq, dk, dv = mha_backward(qp, kp, vp, op, dop, lse.contiguous(), cfg.causal, cfg.scale(),
+                              dropout_p=cfg.dropout_p, seed=cfg.seed)
     d = cfg.head_dim
     return dq[..., :d].contiguous(), dk[..., :d].contiguous(), dv[..., :d].contiguous()
 
@@ -244,25 +246,26 @@ class MHAFunction(torch.autograd.Function):
     """torch.autograd binding: forward = mha_forward, backward = mha_backward."""
 
     @staticmethod
-    def forward(ctx, q, k, v, causal=False, softmax_scale=0.0):
+    def forward(ctx, q, k, v, causal=False, softmax_scale=0.0, dropout_p=0.0, seed=0):
         d = q.shape[-1]
         dn = _native_dim(d)
         qp, kp, vp = (_pad(x.contiguous(), dn) for x in (q, k, v))
         scale = softmax_scale if softmax_scale > 0 else 1.0 / math.sqrt(d)
-        o, lse = mha_forward(qp, kp, vp, causal, scale)
+        o, lse = mha_forward(qp, kp, vp, causal, scale, dropout_p=dropout_p, seed=seed)
         ctx.save_for_backward(qp, kp, vp, o, lse)
-        ctx.causal, ctx.scale, ctx.d = causal, scale, d
+        ctx.causal, ctx.scale, ctx.d, ctx.dropout_p, ctx.seed = causal, scale, d, dropout_p, seed
         return o[..., :d] if dn != d else o
 
     @staticmethod
     def backward(ctx, do):
         qp, kp, vp, o, lse = ctx.saved_tensors
         dop = _pad(do.contiguous(), qp.shape[-1])
-        dq, dk, dv = mha_backward(qp, kp, vp, o, dop, lse, ctx.causal, ctx.scale)
+        dq, dk, dv = mha_backward(qp, kp, vp, o, dop, lse, ctx.causal, ctx.scale,
+                                  dropout_p=ctx.dropout_p, seed=ctx.seed)
         d = ctx.d
-        return dq[..., :d], dk[..., :d], dv[..., :d], None, None
+        return dq[..., :d], dk[..., :d], dv[..., :d], None, None, None, None
 
 
-def attention(q, k, v, causal: bool = False, softmax_scale: float = 0.0):
+def attention(q, k, v, causal: bool = False, softmax_scale: float = 0.0, dropout_p: float = 0.0, seed: int = 0):
     """Differentiable fused attention on [B, H, N, d] fp16/bf16 CUDA tensors."""
-    return MHAFunction.apply(q, k, v, causal, softmax_scale)
+    return MHAFunction.apply(q, k, v, causal, softmax_scale, dropout_p, seed)

@@ -128,6 +128,8 @@ int validate(const vattn_config* c) {
         return fail(VATTN_EINVAL, "vattn_config: dtype must be VATTN_F16 or VATTN_BF16");
     if (c->causal != 0 && c->causal != 1) return fail(VATTN_EINVAL, "vattn_config: causal must be 0/1");
     if (!std::isfinite(c->softmax_scale)) return fail(VATTN_EINVAL, "vattn_config: softmax_scale not finite");
+    if (!(c->dropout_p >= 0.0f && c->dropout_p < 1.0f))
+        return fail(VATTN_EINVAL, "AttnConfig: dropout_p must be in [0, 1)");
     if (c->head_dim != 64 && c->head_dim != 128)
         return fail(VATTN_EUNSUPPORTED, "head_dim must be 64 or 128 at the C ABI (pad in the caller)");
     const long long bh = static_cast<long long>(c->batch) * c->heads;
@@ -145,7 +147,16 @@ float eff_scale(const vattn_config* c) {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-template <int kD, bool kBF16>
+// Dropout constants: keep iff bits_to_unit(hash) >= p  <=>  (hash >> 11) >= ceil(p * 2^53)
+// (exact: bits_to_unit is (hash >> 11) * 2^-53 in binary64, rng.cpp:19-21, 46-49).
+void set_dropout(const vattn_config* c, int* H, float* inv_keep, uint64_t* seed, uint64_t* thresh) {
+    *H = c->heads;
+    *inv_keep = 1.0f / (1.0f - c->dropout_p);  // binary32, attention_forward.cpp:83 / attention_backward.cpp:81
+    *seed = c->seed;
+    *thresh = static_cast<uint64_t>(std::ceil(static_cast<double>(c->dropout_p) * 9007199254740992.0));
+}
+
+template <int kD, bool kBF16, bool kDrop>
 int launch_forward(const vattn_config* c, const void* q, const void* k, const void* v, void* o,
                    float* lse, cudaStream_t stream) {
     const int BH = c->batch * c->heads, N = c->seq_len;
@@ -153,7 +164,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     if (!make_map(&mq, q, BH, N, kD, kBF16) || !make_map(&mk, k, BH, N, kD, kBF16) ||
         !make_map(&mv, v, BH, N, kD, kBF16) || !make_map(&mo, o, BH, N, kD, kBF16))
         return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled failed");
-    auto kern = mha_fwd_sm100_kernel<kD, kBF16>;
+    auto kern = mha_fwd_sm100_kernel<kD, kBF16, kDrop>;
     constexpr int smem = FwdCfg<kD>::kSmemBytes;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -167,6 +178,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     p.n_kv = (N + 127) / 128;
     p.causal = c->causal;
     p.scale_log2 = eff_scale(c) * kLog2e;
+    set_dropout(c, &p.H, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
     dim3 grid((N + 255) / 256, BH);
     {
         ProfScope prof(stream, 0);
@@ -206,7 +218,7 @@ cudaError_t set_smem_once(int bytes) {
     return err;
 }
 
-template <int kD, bool kBF16>
+template <int kD, bool kBF16, bool kDrop>
 int launch_backward(const vattn_config* c, const void* q, const void* k, const void* v,
                     const void* o, const void* dout, const float* lse, void* dq, void* dk,
                     void* dv, void* ws, cudaStream_t stream) {
@@ -239,20 +251,21 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     p.causal = c->causal;
     p.scale = eff_scale(c);
     p.scale_log2 = p.scale * kLog2e;
+    set_dropout(c, &p.H, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
     // 2) dK, dV (key-major)
     {
-        auto kern = mha_bwd_dkdv_kernel<kD, kBF16>;
+        auto kern = mha_bwd_dkdv_kernel<kD, kBF16, kDrop>;
         constexpr int smem = DkdvCfg<kD>::kSmemBytes;
-        const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16>>(smem);
+        const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
         kern<<<dim3(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, dk, dv, p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)
     {
-        auto kern = mha_bwd_dq_kernel<kD, kBF16>;
+        auto kern = mha_bwd_dq_kernel<kD, kBF16, kDrop>;
         constexpr int smem = DqCfg<kD>::kSmemBytes;
-        const cudaError_t ae = set_smem_once<mha_bwd_dq_kernel<kD, kBF16>>(smem);
+        const cudaError_t ae = set_smem_once<mha_bwd_dq_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 2);
         kern<<<dim3(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, mdq, p);
@@ -327,12 +340,17 @@ int mha_forward(const vattn_config* cfg, const void* q, const void* k, const voi
         return fail(VATTN_EINVAL, "mha_forward: tensors must be 16-byte aligned");
     if ((rc = check_device())) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const bool bf = cfg->dtype == VATTN_BF16;
-    if (cfg->head_dim == 64)
-        return bf ? launch_forward<64, true>(cfg, q, k, v, o, lse, s)
-                  : launch_forward<64, false>(cfg, q, k, v, o, lse, s);
-    return bf ? launch_forward<128, true>(cfg, q, k, v, o, lse, s)
-              : launch_forward<128, false>(cfg, q, k, v, o, lse, s);
+    const int sel = (cfg->head_dim == 128 ? 4 : 0) | (cfg->dtype == VATTN_BF16 ? 2 : 0) | (cfg->dropout_p > 0.0f ? 1 : 0);
+    switch (sel) {
+        case 0: return launch_forward<64, false, false>(cfg, q, k, v, o, lse, s);
+        case 1: return launch_forward<64, false, true>(cfg, q, k, v, o, lse, s);
+        case 2: return launch_forward<64, true, false>(cfg, q, k, v, o, lse, s);
+        case 3: return launch_forward<64, true, true>(cfg, q, k, v, o, lse, s);
+        case 4: return launch_forward<128, false, false>(cfg, q, k, v, o, lse, s);
+        case 5: return launch_forward<128, false, true>(cfg, q, k, v, o, lse, s);
+        case 6: return launch_forward<128, true, false>(cfg, q, k, v, o, lse, s);
+        default: return launch_forward<128, true, true>(cfg, q, k, v, o, lse, s);
+    }
 }
 
 size_t mha_backward_workspace_bytes(const vattn_config* cfg) {
@@ -357,12 +375,19 @@ int mha_backward(const vattn_config* cfg, const void* q, const void* k, const vo
         return fail(VATTN_EINVAL, "mha_backward: workspace too small (see mha_backward_workspace_bytes)");
     if ((rc = check_device())) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const bool bf = cfg->dtype == VATTN_BF16;
-    if (cfg->head_dim == 64)
-        return bf ? launch_backward<64, true>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, s)
-                  : launch_backward<64, false>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, s);
-    return bf ? launch_backward<128, true>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, s)
-              : launch_backward<128, false>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, s);
+    const int sel = (cfg->head_dim == 128 ? 4 : 0) | (cfg->dtype == VATTN_BF16 ? 2 : 0) | (cfg->dropout_p > 0.0f ? 1 : 0);
+#define VATTN_BWD(D, BF, DR) launch_backward<D, BF, DR>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, s)
+    switch (sel) {
+        case 0: return VATTN_BWD(64, false, false);
+        case 1: return VATTN_BWD(64, false, true);
+        case 2: return VATTN_BWD(64, true, false);
+        case 3: return VATTN_BWD(64, true, true);
+        case 4: return VATTN_BWD(128, false, false);
+        case 5: return VATTN_BWD(128, false, true);
+        case 6: return VATTN_BWD(128, true, false);
+        default: return VATTN_BWD(128, true, true);
+    }
+#undef VATTN_BWD
 }
 
 }  // extern "C"

@@ -64,6 +64,10 @@ struct BwdParams {
     int causal;
     float scale;        // softmax scale (applied to dK / dQ)
     float scale_log2;   // scale * log2(e)
+    int H;              // heads (dropout hash uses b and h separately)
+    float inv_keep;     // 1 / (1 - dropout_p)
+    uint64_t drop_seed;
+    uint64_t drop_thresh;
 };
 
 // ================================================================ dK / dV ==
@@ -89,13 +93,14 @@ struct DkdvCfg {
     static constexpr int kSmemQ = 2 * kTileBytes;
     static constexpr int kSmemDO = kSmemQ + kStages * kTileBytes;
     static constexpr int kSmemLD = kSmemDO + kStages * kTileBytes;  // [stage][lse2 128 | D 128]
-    static constexpr int kSmemBar = kSmemLD + kStages * 1024;
+    static constexpr int kSmemDrop = kSmemLD + kStages * 1024;      // dropout row hashes [128] x 16 B
+    static constexpr int kSmemBar = kSmemDrop + 2048;
     static constexpr int kNumBars = 16;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr uint32_t kTmemS = 0, kTmemDP = 128, kTmemDV = 256, kTmemDK = 256 + kD;
 };
 
-template <int kD, bool kBF16>
+template <int kD, bool kBF16, bool kDrop>
 __global__ void __launch_bounds__(384, 1)
     mha_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
@@ -113,6 +118,7 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* sQ = smem + Cfg::kSmemQ;
     uint8_t* sDO = smem + Cfg::kSmemDO;
     float* sLD = reinterpret_cast<float*>(smem + Cfg::kSmemLD);
+    DropRow* sDrop = reinterpret_cast<DropRow*>(smem + Cfg::kSmemDrop);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kSmemBar);
     uint64_t* kv_full = bars;
     uint64_t* q_full = bars + 1;          // [kSt]
@@ -247,6 +253,8 @@ __global__ void __launch_bounds__(384, 1)
         const int key = kb * 128 + r;
         const bool key_ok = key < N;
         const float sc = p.scale_log2;
+        uint64_t dbase = 0;
+        if constexpr (kDrop) dbase = drop_bh_base(p.drop_seed, bh / p.H, bh % p.H);
         for (int s = 0; s < n_steps; ++s) {
             const int st = s % kSt;
             const int i = i0 + s;
@@ -261,6 +269,18 @@ __global__ void __launch_bounds__(384, 1)
             tmem_ld32f(tmem + lb + Cfg::kTmemS + 64 * h + 32, pr + 32);
             tmem_wait_ld();
             const int qbase = i * 128 + 64 * h;
+            uint64_t keepm = ~0ull;  // dropout keep bits of this thread's 64 (query, key) positions
+            if constexpr (kDrop) {
+                // row prefixes of the reference hash for this warpgroup's 64 queries
+                named_bar_sync(1 + h, 128);  // previous step's readers are done
+                if ((warp & 3) * 32 + lane < 64)
+                    sDrop[64 * h + (warp & 3) * 32 + lane] = drop_row(dbase, qbase + (warp & 3) * 32 + lane);
+                named_bar_sync(1 + h, 128);
+                keepm = 0;
+#pragma unroll
+                for (int x = 0; x < 64; ++x)
+                    keepm |= static_cast<uint64_t>(drop_keep(sDrop[64 * h + x], key, p.drop_thresh)) << x;
+            }
 #pragma unroll
             for (int x = 0; x < 64; x += 4) {
                 const float4 l4 = *reinterpret_cast<const float4*>(lse2 + x);
@@ -279,8 +299,15 @@ __global__ void __launch_bounds__(384, 1)
             }
             {
                 uint32_t pk[32];
+                if constexpr (kDrop) {  // dV operand f16(P * drop) (attention_backward.cpp:163-167)
 #pragma unroll
-                for (int x = 0; x < 32; ++x) pk[x] = pack2<kBF16>(pr[2 * x], pr[2 * x + 1]);
+                    for (int x = 0; x < 32; ++x)
+                        pk[x] = pack2<kBF16>((keepm >> (2 * x)) & 1 ? pr[2 * x] * p.inv_keep : 0.0f,
+                                             (keepm >> (2 * x + 1)) & 1 ? pr[2 * x + 1] * p.inv_keep : 0.0f);
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) pk[x] = pack2<kBF16>(pr[2 * x], pr[2 * x + 1]);
+                }
                 tmem_st32(tmem + lb + Cfg::kTmemS + 64 * h, pk);  // own columns only
             }
             tmem_wait_st();
@@ -304,7 +331,12 @@ __global__ void __launch_bounds__(384, 1)
                     const float dvv[4] = {d4.x, d4.y, d4.z, d4.w};
                     float ds[4];
 #pragma unroll
-                    for (int y = 0; y < 4; ++y) ds[y] = pr[32 * c + x + y] * (dpv[x + y] - dvv[y]);
+                    for (int y = 0; y < 4; ++y) {
+                        float dpd = dpv[x + y];
+                        if constexpr (kDrop)  // dS = P o (drop o dP - D) (attention_backward.cpp:176-182)
+                            dpd = (keepm >> (32 * c + x + y)) & 1 ? dpd * p.inv_keep : 0.0f;
+                        ds[y] = pr[32 * c + x + y] * (dpd - dvv[y]);
+                    }
                     dsp[16 * c + x / 2] = pack2<kBF16>(ds[0], ds[1]);
                     dsp[16 * c + x / 2 + 1] = pack2<kBF16>(ds[2], ds[3]);
                 }
@@ -384,7 +416,7 @@ struct DqCfg {
     static constexpr uint32_t kTmemDP = 256, kTmemDQ = 384;
 };
 
-template <int kD, bool kBF16>
+template <int kD, bool kBF16, bool kDrop>
 __global__ void __launch_bounds__(384, 1)
     mha_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q,
                       const __grid_constant__ CUtensorMap tm_k,
@@ -559,6 +591,8 @@ __global__ void __launch_bounds__(384, 1)
         const float sc = p.scale_log2;
         const float lse2 = p.lse2[static_cast<size_t>(bh) * p.Npad + q];  // +inf past N
         const float dsum = p.dsum[static_cast<size_t>(bh) * p.Npad + q];
+        DropRow drow{};
+        if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, bh / p.H, bh % p.H), q);
         for (int j = 0; j < nk; ++j) {
             const uint32_t R = (j & 1) ? 128u : 0u;
             mbar_wait<VATTN_SLEEP_MATH>(s_full + (j & 1), (j >> 1) & 1);
@@ -588,6 +622,13 @@ __global__ void __launch_bounds__(384, 1)
                 float dpv[32];
                 tmem_ld32f(tmem + lb + Cfg::kTmemDP + 64 * h + 32 * c, dpv);
                 tmem_wait_ld();
+                if constexpr (kDrop) {  // dS = P o (drop o dP - D)
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) {
+                        const int col = j * 128 + 64 * h + 32 * c + x;
+                        dpv[x] = drop_keep(drow, col, p.drop_thresh) ? dpv[x] * p.inv_keep : 0.0f;
+                    }
+                }
 #pragma unroll
                 for (int x = 0; x < 16; ++x)
                     dsp[16 * c + x] = pack2<kBF16>(pr[32 * c + 2 * x] * (dpv[2 * x] - dsum),

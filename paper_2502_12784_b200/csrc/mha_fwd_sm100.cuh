@@ -32,6 +32,10 @@ struct FwdParams {
     int n_kv;            // ceil(N / 128)
     int causal;
     float scale_log2;    // softmax_scale * log2(e)
+    int H;               // heads (dropout hash uses b and h separately)
+    float inv_keep;      // 1 / (1 - dropout_p), binary32 like the reference
+    uint64_t drop_seed;
+    uint64_t drop_thresh;  // keep iff (hash >> 11) >= drop_thresh
 };
 
 template <int kD>
@@ -48,7 +52,7 @@ struct FwdCfg {
     static constexpr uint32_t kTmemO = 256;
 };
 
-template <int kD, bool kBF16>
+template <int kD, bool kBF16, bool kDrop>
 __global__ void __launch_bounds__(384, 1)
     mha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
@@ -216,6 +220,8 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t tO = tmem + lane_base + Cfg::kTmemO + kD * t;
         const int row = q0 + 128 * t + r;
         const float sc = p.scale_log2;
+        DropRow drow{};
+        if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, bh / p.H, bh % p.H), row);
         float m_run = -INFINITY;  // running max, log2 units (already scaled)
         float l_run = 0.0f;
         const int ntile = nk[t];
@@ -286,8 +292,16 @@ __global__ void __launch_bounds__(384, 1)
                 for (int x = 0; x < 32; ++x) {
                     const float p0 = exp2f_(x, fmaf(s[64 * c + 2 * x], sc, -m_use));
                     const float p1 = exp2f_(x, fmaf(s[64 * c + 2 * x + 1], sc, -m_use));
-                    ls[x & 3] += p0 + p1;
+                    ls[x & 3] += p0 + p1;  // l uses the weights before dropout
                     pk[x] = pack2<kBF16>(p0, p1);
+                    if constexpr (kDrop) {
+                        // dropout on the 16-bit P: f16(f16(P) * 1/(1-p)) or 0
+                        // (attention_forward.cpp:94-106)
+                        const int col = j * 128 + 64 * c + 2 * x;
+                        const float2 f = unpack2<kBF16>(pk[x]);
+                        pk[x] = pack2<kBF16>(drop_keep(drow, col, p.drop_thresh) ? f.x * p.inv_keep : 0.0f,
+                                             drop_keep(drow, col + 1, p.drop_thresh) ? f.y * p.inv_keep : 0.0f);
+                    }
                 }
                 tmem_st32(tS + 32 * c, pk);
                 tmem_wait_st();

@@ -508,6 +508,46 @@ VATTN_DEV void st_swz128(uint8_t* tile, uint32_t row, uint32_t chunk, uint4 v) {
     *reinterpret_cast<uint4*>(tile + off) = v;
 }
 
+// -------------------------------------------------------------- dropout --
+// The reference's stateless dropout decision (proj/src/rng.cpp:35-49):
+//   keep(b,h,row,col) = bits_to_unit(position_hash(seed,b,h,row,col)) >= p
+// with position_hash a chain of SplitMix64 hash_combine over (tag, b, h, row,
+// col).  The (b, h) prefix is computed once per CTA and the row prefix once per
+// row, so each element costs one mix64.  `u >= p` is evaluated exactly in
+// integers: (h >> 11) >= ceil(p * 2^53) (computed on the host).
+VATTN_DEV uint64_t mix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+VATTN_DEV uint64_t hash_combine(uint64_t state, uint64_t v) {
+    return mix64(state ^ (v + 0x9e3779b97f4a7c15ull + (state << 6) + (state >> 2)));
+}
+struct DropRow {
+    uint64_t s;  // hash state after (tag, b, h, row)
+    uint64_t k;  // 0x9e3779b97f4a7c15 + (s << 6) + (s >> 2)
+};
+VATTN_DEV uint64_t drop_bh_base(uint64_t seed, int b, int h) {
+    return hash_combine(hash_combine(hash_combine(seed, 0x64726f70ull), static_cast<uint64_t>(b)),
+                        static_cast<uint64_t>(h));
+}
+VATTN_DEV DropRow drop_row(uint64_t bh_base, int row) {
+    DropRow r;
+    r.s = hash_combine(bh_base, static_cast<uint64_t>(row));
+    r.k = 0x9e3779b97f4a7c15ull + (r.s << 6) + (r.s >> 2);
+    return r;
+}
+VATTN_DEV bool drop_keep(const DropRow& r, int col, uint64_t thresh) {
+    return (mix64(r.s ^ (static_cast<uint64_t>(col) + r.k)) >> 11) >= thresh;
+}
+// Round to the 16-bit storage type and back (the reference narrows P once
+// before dropout and once after the 1/(1-p) scaling, attention_forward.cpp:94-106).
+template <bool kBF16>
+VATTN_DEV float round16(float x) {
+    return unpack2<kBF16>(pack2<kBF16>(x, 0.0f)).x;
+}
+
 // ------------------------------------------------ global-memory ordering --
 
 VATTN_DEV int ld_acquire_gpu(const int* p) {

@@ -50,7 +50,8 @@ def test_sm100a_code_only():
 
 class Cfg(C.Structure):
     _fields_ = [("batch", C.c_int32), ("heads", C.c_int32), ("seq_len", C.c_int32), ("head_dim", C.c_int32),
-                ("causal", C.c_int32), ("softmax_scale", C.c_float), ("dtype", C.c_int32)]
+                ("causal", C.c_int32), ("softmax_scale", C.c_float), ("dtype", C.c_int32),
+                ("dropout_p", C.c_float), ("seed", C.c_uint64)]
 
 
 def test_validation_matches_reference_errors(lib):
@@ -60,7 +61,8 @@ def test_validation_matches_reference_errors(lib):
     lib.mha_backward_workspace_bytes.restype = C.c_size_t
     EINVAL, EUNSUP, ECUDA = 1, 3, 4
     bad = [Cfg(0, 1, 64, 64, 0, 0.0, 0), Cfg(1, 1, 0, 64, 0, 0.0, 0), Cfg(1, 1, 64, 64, 2, 0.0, 0),
-           Cfg(1, 1, 64, 64, 0, 0.0, 7), Cfg(1, 1, 64, 64, 0, float("nan"), 0)]
+           Cfg(1, 1, 64, 64, 0, 0.0, 7), Cfg(1, 1, 64, 64, 0, float("nan"), 0),
+           Cfg(1, 1, 64, 64, 0, 0.0, 0, 1.0, 0), Cfg(1, 1, 64, 64, 0, 0.0, 0, -0.1, 0)]
     for c in bad:
         assert lib.mha_forward(C.byref(c), 16, 16, 16, 16, 16, None) == EINVAL
         assert lib.mha_backward_workspace_bytes(C.byref(c)) == 0
@@ -93,4 +95,4 @@ def test_python_mirror_config_validation():
         vb.AttnConfig(seq_len=64, head_dim=64, dropout_p=1.0).validate()
     vb.AttnConfig(seq_len=100, head_dim=64).validate(strict_tiles=False)
     assert abs(vb.AttnConfig(seq_len=64, head_dim=64).scale() - 0.125) < 1e-9
-    assert vb.lib.vattn_abi_version() == 1
+    assert vb.lib.vattn_abi_version() == 2

@@ -218,7 +218,67 @@ def test_error_paths():
         vb.forward_fused(big, big, big, vb.AttnConfig(seq_len=64, head_dim=256))
     with pytest.raises(ValueError):
         vb.AttnConfig(seq_len=100, head_dim=64).validate()  # N not a tile multiple (reference rule)
-    with pytest.raises(NotImplementedError):
-        vb.forward_fused(q, q, q, vb.AttnConfig(seq_len=64, head_dim=64, dropout_p=0.1))
+    with pytest.raises(ValueError):
+        vb.forward_fused(q, q, q, vb.AttnConfig(seq_len=64, head_dim=64, dropout_p=1.0))
     with pytest.raises(ValueError):
         vb.mha_forward(q.cpu(), q.cpu(), q.cpu())
+
+
+# ---------------------------------------------------------------- dropout --
+DROP = json.load(open(os.path.join(GOLDEN, "manifest.json")))["dropout_cases"]
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_dropout_mask_bitwise_vs_reference(causal, dtype):
+    """Q = K = 0 and V = I make O the dropped-out P itself: every keep bit must be
+    the reference's dropout_keep(seed, b, h, row, col, p) (rng.cpp:46-49)."""
+    B, H, N, d, p, seed = 2, 2, 64, 64, 0.3, 987654321
+    q = torch.zeros(B, H, N, d, dtype=dtype, device="cuda")
+    v = torch.eye(N, d, dtype=dtype, device="cuda").expand(B, H, N, d).contiguous()
+    o, _ = vb.mha_forward(q, q, v, causal, dropout_p=p, seed=seed)
+    kept = (o != 0).cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            want = np.array([[po.dropout_keep(seed, b, h, i, j, p) and (not causal or j <= i) for j in range(N)]
+                             for i in range(N)])
+            assert np.array_equal(kept[b, h], want), (b, h)
+
+
+@pytest.mark.parametrize("case", DROP, ids=[c["name"] for c in DROP])
+def test_dropout_golden_forward_backward(case):
+    g = golden(case["name"])
+    B, H, N, d = case["shape"]
+    p, ds = case["dropout_p"], case["dropout_seed"]
+    q, k, v, do = (bits_to_torch(g[x]) for x in ("q", "k", "v", "dout"))
+    cfg = vb.AttnConfig(batch=B, heads=H, seq_len=N, head_dim=d, causal=case["causal"], dropout_p=p, seed=ds)
+    out, lse = vb.forward_fused(q, k, v, cfg)
+    dq, dk, dv = vb.backward_fused(q, k, v, do, lse, cfg, out=out)
+    torch.cuda.synchronize()
+    check_close(widen(out), g["ref_out"], torch.float16, "O vs binary64 (dropout)")
+    check_close(widen(out), po.widen(g["fwd32_out"]), torch.float16, "O vs forward_fused (dropout)")
+    check_lse(lse.cpu().double().numpy(), g["ref_lse"])
+    for name, t in (("dq", dq), ("dk", dk), ("dv", dv)):
+        check_close(widen(t), g["ref_" + name], torch.float16, f"{name} vs binary64 (dropout)")
+        check_close(widen(t), po.widen(g["bwd16_" + name]), torch.float16, f"{name} vs backward_fused (dropout)",
+                    fro=3e-3, abs_=1e-2)
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,dtype", [(1, 2, 256, 128, True, torch.bfloat16),
+                                                  (2, 1, 200, 64, False, torch.float16)])
+def test_dropout_random_vs_binary64_and_deterministic(B, H, N, d, causal, dtype):
+    q, k, v, do = workload(31, (B, H, N, d), dtype)
+    p, seed = 0.1, 2025
+    o, lse = vb.mha_forward(q, k, v, causal, dropout_p=p, seed=seed)
+    dq, dk, dv = vb.mha_backward(q, k, v, o, do, lse, causal, dropout_p=p, seed=seed)
+    qd, kd, vd, dod = (widen(x) for x in (q, k, v, do))
+    ro, rlse = po.attention_ref(qd, kd, vd, causal, dropout_p=p, seed=seed)
+    check_close(widen(o), ro, dtype, "O")
+    check_lse(lse.cpu().double().numpy(), rlse)
+    rdq, rdk, rdv = po.attention_grad_ref(qd, kd, vd, dod, causal, dropout_p=p, seed=seed)
+    check_close(widen(dq), rdq, dtype, "dQ")
+    check_close(widen(dk), rdk, dtype, "dK")
+    check_close(widen(dv), rdv, dtype, "dV")
+    o2, _ = vb.mha_forward(q, k, v, causal, dropout_p=p, seed=seed)
+    g2 = vb.mha_backward(q, k, v, o, do, lse, causal, dropout_p=p, seed=seed)
+    assert torch.equal(o, o2) and all(torch.equal(a, b) for a, b in zip((dq, dk, dv), g2))
