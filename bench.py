@@ -212,10 +212,13 @@ def main():
     ws = torch.empty(vb.workspace_bytes(B, H, N, d, causal, dtype), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
+    # this rank's (b, h) slab of the global [B*world, H] problem (dropout masks use global (b, h))
+    slab = (B * world, H, rank * B * H, B * H) if world > 1 else None
+
     def step():
-        vb.mha_forward(q, k, v, causal, out=o, lse=lse, dropout_p=args.dropout, seed=1234)
+        vb.mha_forward(q, k, v, causal, out=o, lse=lse, dropout_p=args.dropout, seed=1234, bh_slab=slab)
         vb.mha_backward(q, k, v, o, do, lse, causal, dq=dq, dk=dk, dv=dv, workspace=ws,
-                        dropout_p=args.dropout, seed=1234)
+                        dropout_p=args.dropout, seed=1234, bh_slab=slab)
 
     for _ in range(args.warmup):
         step()
@@ -253,7 +256,9 @@ def main():
     value = world * (f_fwd + f_bwd) / (ms_step * 1e-3) / 1e12
 
     # ------------------------------------------------------------------ e2e
-    # Public API with host buffers: pinned H2D of Q, K, V, dO; D2H of O, lse, dQ, dK, dV.
+    # Public API with host buffers: mha_step_host (C ABI) takes pinned host Q, K, V, dO
+    # and returns O, lse, dQ, dK, dV in host memory; the H2D / D2H copies run inside
+    # the call (pipelined against the kernels slab by slab).
     hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, do))
     ho, hdq, hdk, hdv = (torch.empty(shape, dtype=dtype).pin_memory() for _ in range(4))
     hlse = torch.empty((B, H, N), dtype=torch.float32).pin_memory()
@@ -261,32 +266,26 @@ def main():
     d2h = sum(x.numel() * x.element_size() for x in (ho, hlse, hdq, hdk, hdv))
 
     def e2e_step():
-        q.copy_(hq, non_blocking=True)
-        k.copy_(hk, non_blocking=True)
-        v.copy_(hv, non_blocking=True)
-        do.copy_(hdo, non_blocking=True)
-        step()
-        ho.copy_(o, non_blocking=True)
-        hlse.copy_(lse, non_blocking=True)
-        hdq.copy_(dq, non_blocking=True)
-        hdk.copy_(dk, non_blocking=True)
-        hdv.copy_(dv, non_blocking=True)
+        vb.mha_step_host(hq, hk, hv, hdo, causal, dropout_p=args.dropout, seed=1234,
+                         out=(ho, hlse, hdq, hdk, hdv))
 
-    e2e_step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.e2e_steps):
+    e2e_ms = e2e_val = None
+    if args.e2e_steps > 0:
         e2e_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    te = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = te.item() / args.e2e_steps
-    e2e_val = world * (f_fwd + f_bwd) / (e2e_ms * 1e-3) / 1e12
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = te.item() / args.e2e_steps
+        e2e_val = world * (f_fwd + f_bwd) / (e2e_ms * 1e-3) / 1e12
 
     if rank == 0:
         peak_burst, peak_sust, peak_src = measured_peaks()

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define VATTN_B200_ABI_VERSION 2
+#define VATTN_B200_ABI_VERSION 3
 
 typedef enum vattn_status {
     VATTN_OK = 0,
@@ -71,6 +71,16 @@ typedef struct vattn_config {
     float dropout_p;        /* in [0, 1); 0 = no dropout (AttnConfig::dropout_p)   */
     uint64_t seed;          /* dropout seed: keep masks are bit-identical to the
                                reference's dropout_keep(seed, b, h, row, col, p)   */
+    int32_t bh_offset;      /* (batch, head) slab of the problem this call runs:   */
+    int32_t bh_count;       /* units [bh_offset, bh_offset + bh_count) of the      */
+                            /* flattened b*H + h axis; the tensor pointers point at
+                               unit bh_offset.  bh_count = 0 selects the whole
+                               problem (bh_offset must then be 0).  Units are
+                               independent, so a slab's outputs are bit-identical
+                               to the same units of a whole-problem call (dropout
+                               masks use the global (b, h)).  This is how ranks
+                               shard the path and how the host API
+                               pipelines PCIe copies against compute.             */
 } vattn_config;
 
 /* O = softmax(Q K^T * scale [+ causal mask]) V ;  lse = logsumexp per query row. */
@@ -87,6 +97,32 @@ size_t mha_backward_workspace_bytes(const vattn_config* cfg);
 int mha_backward(const vattn_config* cfg, const void* q, const void* k, const void* v,
                  const void* o, const void* dout, const float* lse, void* dq, void* dk, void* dv,
                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- host-buffer entry points (the reference's synchronous host API) ------
+ * Same math as the device entry points, but every tensor is a HOST pointer
+ * (pinned memory gives full copy/compute overlap; pageable memory works but
+ * the copies serialise).  The call splits the (b, h) units into slabs and
+ * pipelines them over three streams -- H2D of slab c+1, the kernels of slab c
+ * (on `stream`), D2H of slab c-1 -- so PCIe traffic in both directions overlaps
+ * the sm_100a kernels.  Device staging comes from a library-owned stream-ordered
+ * pool.  Synchronous: outputs are valid when the call returns (like
+ * vattn::forward_fused / backward_fused).  Results are bit-identical to the
+ * device entry points. */
+
+/* vattn::forward_fused on host buffers: O, lse. */
+int mha_forward_host(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o,
+                     float* lse, void* stream);
+
+/* vattn::backward_fused on host buffers (O given, see the divergence note). */
+int mha_backward_host(const vattn_config* cfg, const void* q, const void* k, const void* v,
+                      const void* o, const void* dout, const float* lse, void* dq, void* dk,
+                      void* dv, void* stream);
+
+/* One attention training step on host buffers: forward then backward with Q, K,
+ * V and dO crossing PCIe once, O, lse, dQ, dK, dV returned. */
+int mha_step_host(const vattn_config* cfg, const void* q, const void* k, const void* v,
+                  const void* dout, void* o, float* lse, void* dq, void* dk, void* dv,
+                  void* stream);
 
 /* Thread-local description of the last failure on this thread ("" if none). */
 const char* vattn_last_error(void);

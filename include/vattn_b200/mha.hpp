@@ -126,7 +126,7 @@ inline void download_padded(uint16_t* dst, const void* src, size_t rows, int d, 
 }
 
 inline vattn_config to_c(const AttnConfig& c, int dn) {
-    vattn_config r;
+    vattn_config r{};  // bh_offset = bh_count = 0: the whole problem
     r.batch = c.batch;
     r.heads = c.heads;
     r.seq_len = c.seq_len;
@@ -166,7 +166,9 @@ inline void backward_fused_device(const AttnConfig& cfg, const void* q, const vo
 
 // ------------------------------------------------------------ host overloads
 
-// vattn::forward_fused: host [B,H,N,d] binary16 in, ForwardOutput out.
+// vattn::forward_fused: host [B,H,N,d] binary16 in, ForwardOutput out.  Native
+// head dims go through mha_forward_host (PCIe copies pipelined against the
+// kernels, slab by slab); other head dims are zero-padded on the device.
 inline ForwardOutput forward_fused(const std::vector<uint16_t>& q, const std::vector<uint16_t>& k,
                                    const std::vector<uint16_t>& v, const AttnConfig& cfg) {
     cfg.validate();
@@ -174,17 +176,22 @@ inline ForwardOutput forward_fused(const std::vector<uint16_t>& q, const std::ve
         throw std::invalid_argument("forward_fused: Q/K/V shape mismatch");
     const int dn = detail::native_dim(cfg.head_dim);
     const size_t rows = cfg.rows();
+    ForwardOutput r;
+    r.out.resize(cfg.elems());
+    r.lse.resize(rows);
+    const vattn_config c = detail::to_c(cfg, dn);
+    if (dn == cfg.head_dim) {
+        detail::check(mha_forward_host(&c, q.data(), k.data(), v.data(), r.out.data(), r.lse.data(), nullptr),
+                      "mha_forward_host");
+        return r;
+    }
     cudaStream_t s = nullptr;
     detail::DevBuf dq(rows * dn * 2), dk(rows * dn * 2), dv(rows * dn * 2), dout(rows * dn * 2),
         dlse(rows * 4);
     detail::upload_padded(dq.p, q.data(), rows, cfg.head_dim, dn, s);
     detail::upload_padded(dk.p, k.data(), rows, cfg.head_dim, dn, s);
     detail::upload_padded(dv.p, v.data(), rows, cfg.head_dim, dn, s);
-    const vattn_config c = detail::to_c(cfg, dn);
     detail::check(mha_forward(&c, dq.p, dk.p, dv.p, dout.p, static_cast<float*>(dlse.p), s), "mha_forward");
-    ForwardOutput r;
-    r.out.resize(cfg.elems());
-    r.lse.resize(rows);
     detail::download_padded(r.out.data(), dout.p, rows, cfg.head_dim, dn, s);
     detail::cuda(cudaMemcpyAsync(r.lse.data(), dlse.p, rows * 4, cudaMemcpyDeviceToHost, s), "D2H lse");
     detail::cuda(cudaStreamSynchronize(s), "sync");

@@ -32,6 +32,7 @@ import torch
 __all__ = [
     "AttnConfig", "forward_fused", "backward_fused", "mha_forward", "mha_backward",
     "workspace_bytes", "MHAFunction", "attention", "LIB_PATH", "lib",
+    "mha_forward_host", "mha_backward_host", "mha_step_host",
 ]
 
 LIB_PATH = os.environ.get("VATTN_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvattn_b200.so")
@@ -44,7 +45,7 @@ class _Cfg(C.Structure):
     _fields_ = [
         ("batch", C.c_int32), ("heads", C.c_int32), ("seq_len", C.c_int32), ("head_dim", C.c_int32),
         ("causal", C.c_int32), ("softmax_scale", C.c_float), ("dtype", C.c_int32),
-        ("dropout_p", C.c_float), ("seed", C.c_uint64),
+        ("dropout_p", C.c_float), ("seed", C.c_uint64), ("bh_offset", C.c_int32), ("bh_count", C.c_int32),
     ]
 
 
@@ -61,6 +62,12 @@ def _load():
     lib.mha_backward_workspace_bytes.restype = C.c_size_t
     lib.mha_backward.argtypes = [C.POINTER(_Cfg)] + [vp] * 10 + [C.c_size_t, vp]
     lib.mha_backward.restype = C.c_int
+    lib.mha_forward_host.argtypes = [C.POINTER(_Cfg)] + [vp] * 6
+    lib.mha_forward_host.restype = C.c_int
+    lib.mha_backward_host.argtypes = [C.POINTER(_Cfg)] + [vp] * 10
+    lib.mha_backward_host.restype = C.c_int
+    lib.mha_step_host.argtypes = [C.POINTER(_Cfg)] + [vp] * 10
+    lib.mha_step_host.restype = C.c_int
     lib.vattn_last_error.restype = C.c_char_p
     lib.vattn_abi_version.restype = C.c_int
     lib.vattn_last_launch_count.restype = C.c_int
@@ -127,9 +134,18 @@ def _dtype_code(t: torch.Tensor) -> int:
     raise ValueError(f"tensors must be float16 or bfloat16, got {t.dtype}")
 
 
-def _cfg(q: torch.Tensor, causal: bool, softmax_scale: float, dropout_p: float = 0.0, seed: int = 0) -> _Cfg:
-    B, H, N, d = q.shape
-    return _Cfg(B, H, N, d, 1 if causal else 0, float(softmax_scale), _dtype_code(q), float(dropout_p), int(seed))
+def _cfg(q: torch.Tensor, causal: bool, softmax_scale: float, dropout_p: float = 0.0, seed: int = 0,
+         bh_slab: tuple[int, int, int, int] | None = None) -> _Cfg:
+    """bh_slab = (B, H, bh_offset, bh_count): q is the [bh_count, 1, N, d] slab of a
+    global (B, H) problem (dropout masks then use the global (b, h))."""
+    if bh_slab is None:
+        B, H, N, d = q.shape
+        off = cnt = 0
+    else:
+        B, H, off, cnt = bh_slab
+        N, d = q.shape[-2:]
+    return _Cfg(B, H, N, d, 1 if causal else 0, float(softmax_scale), _dtype_code(q), float(dropout_p), int(seed),
+                int(off), int(cnt))
 
 
 def _check(ts, shape, dtype, names):
@@ -161,7 +177,7 @@ def _pad(t: torch.Tensor, dn: int) -> torch.Tensor:
 
 
 def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=None, lse=None,
-                dropout_p: float = 0.0, seed: int = 0):
+                dropout_p: float = 0.0, seed: int = 0, bh_slab=None):
     """C ABI ``mha_forward`` on CUDA tensors [B, H, N, d] (d in {64, 128}).
     Returns (out, lse) with lse [B, H, N] fp32 natural-log.  ``dropout_p > 0``
     applies the reference's dropout (keep bits = vattn::dropout_keep(seed, b, h, row, col, p))."""
@@ -169,7 +185,7 @@ def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=N
     B, H, N, d = q.shape
     out = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
-    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
     rc = lib.mha_forward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                          lse.data_ptr(), _stream())
     if rc:
@@ -178,18 +194,20 @@ def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=N
 
 
 def workspace_bytes(B, H, N, d, causal=False, dtype=torch.float16) -> int:
-    cfg = _Cfg(B, H, N, d, 1 if causal else 0, 0.0, VATTN_BF16 if dtype == torch.bfloat16 else VATTN_F16, 0.0, 0)
+    cfg = _Cfg(B, H, N, d, 1 if causal else 0, 0.0, VATTN_BF16 if dtype == torch.bfloat16 else VATTN_F16, 0.0, 0, 0, 0)
     return int(lib.mha_backward_workspace_bytes(C.byref(cfg)))
 
 
 def mha_backward(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: float = 0.0,
-                 dq=None, dk=None, dv=None, workspace=None, dropout_p: float = 0.0, seed: int = 0):
-    """C ABI ``mha_backward`` on CUDA tensors.  Returns (dq, dk, dv)."""
+                 dq=None, dk=None, dv=None, workspace=None, dropout_p: float = 0.0, seed: int = 0, bh_slab=None):
+    """C ABI ``mha_backward`` on CUDA tensors.  Returns (dq, dk, dv).
+    ``bh_slab=(B, H, offset, count)``: the tensors are units [offset, offset+count)
+    of a global (B, H) problem (used by (b, h) sharding)."""
     _check((q, k, v, o, dout), q.shape, q.dtype, ("q", "k", "v", "o", "dout"))
     B, H, N, d = q.shape
     if lse.shape != (B, H, N) or lse.dtype != torch.float32 or not lse.is_contiguous():
         raise ValueError("lse must be a contiguous float32 [B, H, N] tensor")
-    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
     need = int(lib.mha_backward_workspace_bytes(C.byref(cfg)))
     if need == 0:
         rc = lib.mha_backward(C.byref(cfg), *([None] * 10), 0, None)
@@ -205,6 +223,72 @@ def mha_backward(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: flo
     if rc:
         _raise(rc, "mha_backward")
     return dq, dk, dv
+
+
+# -------------------------------------------------- host-buffer entry points --
+
+def _check_host(ts, shape, dtype, names):
+    for t, n in zip(ts, names):
+        if tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+            raise ValueError(f"{n}: expected {dtype} {tuple(shape)}, got {t.dtype} {tuple(t.shape)}")
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{n} must be a contiguous host (CPU) tensor")
+
+
+def _host_empty(shape, dtype, like):
+    t = torch.empty(shape, dtype=dtype)
+    return t.pin_memory() if like.is_pinned() else t
+
+
+def mha_forward_host(q, k, v, causal: bool = False, softmax_scale: float = 0.0, dropout_p: float = 0.0,
+                     seed: int = 0, out=None, lse=None):
+    """C ABI ``mha_forward_host``: host tensors in and out, PCIe copies pipelined
+    against the kernels slab by slab.  Pinned inputs give full overlap."""
+    _check_host((q, k, v), q.shape, q.dtype, ("q", "k", "v"))
+    B, H, N, d = q.shape
+    out = _host_empty(q.shape, q.dtype, q) if out is None else out
+    lse = _host_empty((B, H, N), torch.float32, q) if lse is None else lse
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
+    rc = lib.mha_forward_host(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                              lse.data_ptr(), _stream())
+    if rc:
+        _raise(rc, "mha_forward_host")
+    return out, lse
+
+
+def mha_backward_host(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: float = 0.0,
+                      dropout_p: float = 0.0, seed: int = 0, dq=None, dk=None, dv=None):
+    """C ABI ``mha_backward_host`` on host tensors.  Returns (dq, dk, dv)."""
+    _check_host((q, k, v, o, dout), q.shape, q.dtype, ("q", "k", "v", "o", "dout"))
+    B, H, N, d = q.shape
+    _check_host((lse,), (B, H, N), torch.float32, ("lse",))
+    dq, dk, dv = (_host_empty(q.shape, q.dtype, q) if t is None else t for t in (dq, dk, dv))
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
+    rc = lib.mha_backward_host(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                               dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                               _stream())
+    if rc:
+        _raise(rc, "mha_backward_host")
+    return dq, dk, dv
+
+
+def mha_step_host(q, k, v, dout, causal: bool = False, softmax_scale: float = 0.0, dropout_p: float = 0.0,
+                  seed: int = 0, out=None):
+    """C ABI ``mha_step_host``: forward + backward on host tensors with Q, K, V, dO
+    crossing PCIe once.  ``out`` = optional preallocated (o, lse, dq, dk, dv).
+    Returns (o, lse, dq, dk, dv)."""
+    _check_host((q, k, v, dout), q.shape, q.dtype, ("q", "k", "v", "dout"))
+    B, H, N, d = q.shape
+    if out is None:
+        out = (_host_empty(q.shape, q.dtype, q), _host_empty((B, H, N), torch.float32, q),
+               *(_host_empty(q.shape, q.dtype, q) for _ in range(3)))
+    o, lse, dq, dk, dv = out
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
+    rc = lib.mha_step_host(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), o.data_ptr(),
+                           lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), _stream())
+    if rc:
+        _raise(rc, "mha_step_host")
+    return o, lse, dq, dk, dv
 
 
 # ----------------------------------------- reference-shaped operator API --

@@ -132,12 +132,22 @@ int validate(const vattn_config* c) {
         return fail(VATTN_EINVAL, "AttnConfig: dropout_p must be in [0, 1)");
     if (c->head_dim != 64 && c->head_dim != 128)
         return fail(VATTN_EUNSUPPORTED, "head_dim must be 64 or 128 at the C ABI (pad in the caller)");
-    const long long bh = static_cast<long long>(c->batch) * c->heads;
-    if (bh > 65535) return fail(VATTN_EUNSUPPORTED, "batch * heads must be <= 65535");
+    const long long bh_all = static_cast<long long>(c->batch) * c->heads;
+    if (c->bh_count < 0 || c->bh_offset < 0)
+        return fail(VATTN_EINVAL, "vattn_config: bh_offset / bh_count must be >= 0");
+    if (c->bh_count == 0 && c->bh_offset != 0)
+        return fail(VATTN_EINVAL, "vattn_config: bh_offset without bh_count");
+    if (static_cast<long long>(c->bh_offset) + c->bh_count > bh_all)
+        return fail(VATTN_EINVAL, "vattn_config: (b, h) slab [bh_offset, bh_offset + bh_count) exceeds batch * heads");
+    const long long bh = c->bh_count ? c->bh_count : bh_all;
+    if (bh > 65535) return fail(VATTN_EUNSUPPORTED, "batch * heads (per call) must be <= 65535");
     if (bh * c->seq_len > (1ll << 31) - 1)
         return fail(VATTN_EUNSUPPORTED, "batch * heads * seq_len must fit in int32");
     return VATTN_OK;
 }
+
+// (b, h) units this call runs (the slab, or the whole problem).
+int units(const vattn_config* c) { return c->bh_count ? c->bh_count : c->batch * c->heads; }
 
 float eff_scale(const vattn_config* c) {
     // AttnConfig::scale(), proj/src/attention_forward.cpp:42-45
@@ -149,8 +159,9 @@ constexpr float kLog2e = 1.4426950408889634f;
 
 // Dropout constants: keep iff bits_to_unit(hash) >= p  <=>  (hash >> 11) >= ceil(p * 2^53)
 // (exact: bits_to_unit is (hash >> 11) * 2^-53 in binary64, rng.cpp:19-21, 46-49).
-void set_dropout(const vattn_config* c, int* H, float* inv_keep, uint64_t* seed, uint64_t* thresh) {
+void set_dropout(const vattn_config* c, int* H, int* bh_off, float* inv_keep, uint64_t* seed, uint64_t* thresh) {
     *H = c->heads;
+    *bh_off = c->bh_offset;
     *inv_keep = 1.0f / (1.0f - c->dropout_p);  // binary32, attention_forward.cpp:83 / attention_backward.cpp:81
     *seed = c->seed;
     *thresh = static_cast<uint64_t>(std::ceil(static_cast<double>(c->dropout_p) * 9007199254740992.0));
@@ -159,7 +170,7 @@ void set_dropout(const vattn_config* c, int* H, float* inv_keep, uint64_t* seed,
 template <int kD, bool kBF16, bool kDrop>
 int launch_forward(const vattn_config* c, const void* q, const void* k, const void* v, void* o,
                    float* lse, cudaStream_t stream) {
-    const int BH = c->batch * c->heads, N = c->seq_len;
+    const int BH = units(c), N = c->seq_len;
     CUtensorMap mq, mk, mv, mo;
     if (!make_map(&mq, q, BH, N, kD, kBF16) || !make_map(&mk, k, BH, N, kD, kBF16) ||
         !make_map(&mv, v, BH, N, kD, kBF16) || !make_map(&mo, o, BH, N, kD, kBF16))
@@ -178,7 +189,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     p.n_kv = (N + 127) / 128;
     p.causal = c->causal;
     p.scale_log2 = eff_scale(c) * kLog2e;
-    set_dropout(c, &p.H, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
+    set_dropout(c, &p.H, &p.bh_off, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
     dim3 grid((N + 255) / 256, BH);
     {
         ProfScope prof(stream, 0);
@@ -199,7 +210,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 BwdLayout bwd_layout(const vattn_config* c) {
     BwdLayout L{};
-    const size_t BH = static_cast<size_t>(c->batch) * c->heads;
+    const size_t BH = static_cast<size_t>(units(c));
     L.n_q = (c->seq_len + 127) / 128;
     L.Npad = L.n_q * 128;
     L.lse2 = 0;
@@ -222,7 +233,7 @@ template <int kD, bool kBF16, bool kDrop>
 int launch_backward(const vattn_config* c, const void* q, const void* k, const void* v,
                     const void* o, const void* dout, const float* lse, void* dq, void* dk,
                     void* dv, void* ws, cudaStream_t stream) {
-    const int BH = c->batch * c->heads, N = c->seq_len;
+    const int BH = units(c), N = c->seq_len;
     const BwdLayout L = bwd_layout(c);
     uint8_t* w = static_cast<uint8_t*>(ws);
     float* lse2 = reinterpret_cast<float*>(w + L.lse2);
@@ -251,7 +262,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     p.causal = c->causal;
     p.scale = eff_scale(c);
     p.scale_log2 = p.scale * kLog2e;
-    set_dropout(c, &p.H, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
+    set_dropout(c, &p.H, &p.bh_off, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
     // 2) dK, dV (key-major)
     {
         auto kern = mha_bwd_dkdv_kernel<kD, kBF16, kDrop>;
@@ -300,6 +311,11 @@ int vattn_trace_read(long long* out, int n) {
 int vattn_abi_version(void) { return VATTN_B200_ABI_VERSION; }
 
 const char* vattn_last_error(void) { return g_err.c_str(); }
+
+// internal (capi_host.cu): report a host-pipeline failure through vattn_last_error,
+// and validate a config with the device entry points' own rules.
+void vattn_set_error_(const char* msg) { g_err = msg ? msg : ""; }
+int vattn_validate_(const vattn_config* cfg) { return validate(cfg); }
 
 int vattn_last_launch_count(void) { return g_launches; }
 

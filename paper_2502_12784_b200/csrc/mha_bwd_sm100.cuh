@@ -65,6 +65,7 @@ struct BwdParams {
     float scale;        // softmax scale (applied to dK / dQ)
     float scale_log2;   // scale * log2(e)
     int H;              // heads (dropout hash uses b and h separately)
+    int bh_off;         // global index of this launch's first (b, h) unit (slabs)
     float inv_keep;     // 1 / (1 - dropout_p)
     uint64_t drop_seed;
     uint64_t drop_thresh;
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(384, 1)
         const bool key_ok = key < N;
         const float sc = p.scale_log2;
         uint64_t dbase = 0;
-        if constexpr (kDrop) dbase = drop_bh_base(p.drop_seed, bh / p.H, bh % p.H);
+        if constexpr (kDrop) dbase = drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H);
         for (int s = 0; s < n_steps; ++s) {
             const int st = s % kSt;
             const int i = i0 + s;
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(384, 1)
         const float lse2 = p.lse2[static_cast<size_t>(bh) * p.Npad + q];  // +inf past N
         const float dsum = p.dsum[static_cast<size_t>(bh) * p.Npad + q];
         DropRow drow{};
-        if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, bh / p.H, bh % p.H), q);
+        if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H), q);
         for (int j = 0; j < nk; ++j) {
             const uint32_t R = (j & 1) ? 128u : 0u;
             mbar_wait<VATTN_SLEEP_MATH>(s_full + (j & 1), (j >> 1) & 1);

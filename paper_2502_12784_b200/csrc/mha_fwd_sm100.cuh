@@ -33,6 +33,7 @@ struct FwdParams {
     int causal;
     float scale_log2;    // softmax_scale * log2(e)
     int H;               // heads (dropout hash uses b and h separately)
+    int bh_off;          // global index of this launch's first (b, h) unit (slabs)
     float inv_keep;      // 1 / (1 - dropout_p), binary32 like the reference
     uint64_t drop_seed;
     uint64_t drop_thresh;  // keep iff (hash >> 11) >= drop_thresh
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(384, 1)
         const int row = q0 + 128 * t + r;
         const float sc = p.scale_log2;
         DropRow drow{};
-        if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, bh / p.H, bh % p.H), row);
+        if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H), row);
         float m_run = -INFINITY;  // running max, log2 units (already scaled)
         float l_run = 0.0f;
         const int ntile = nk[t];

@@ -27,7 +27,8 @@ def lib():
 
 def test_header_declares_the_boundary():
     fns = declared_functions()
-    for f in ("mha_forward", "mha_backward", "mha_backward_workspace_bytes", "vattn_last_error"):
+    for f in ("mha_forward", "mha_backward", "mha_backward_workspace_bytes", "vattn_last_error",
+              "mha_forward_host", "mha_backward_host", "mha_step_host"):
         assert f in fns, fns
 
 
@@ -51,7 +52,7 @@ def test_sm100a_code_only():
 class Cfg(C.Structure):
     _fields_ = [("batch", C.c_int32), ("heads", C.c_int32), ("seq_len", C.c_int32), ("head_dim", C.c_int32),
                 ("causal", C.c_int32), ("softmax_scale", C.c_float), ("dtype", C.c_int32),
-                ("dropout_p", C.c_float), ("seed", C.c_uint64)]
+                ("dropout_p", C.c_float), ("seed", C.c_uint64), ("bh_offset", C.c_int32), ("bh_count", C.c_int32)]
 
 
 def test_validation_matches_reference_errors(lib):
@@ -78,6 +79,20 @@ def test_validation_matches_reference_errors(lib):
     assert rc in (ECUDA,) or os.environ.get("CUDA_VISIBLE_DEVICES") not in (None, "")
 
 
+def test_slab_validation(lib):
+    """(b, h) slabs: [bh_offset, bh_offset + bh_count) must lie inside B*H."""
+    lib.mha_backward_workspace_bytes.argtypes = [C.POINTER(Cfg)]
+    lib.mha_backward_workspace_bytes.restype = C.c_size_t
+    lib.mha_forward_host.argtypes = [C.POINTER(Cfg)] + [C.c_void_p] * 6
+    whole = lib.mha_backward_workspace_bytes(C.byref(Cfg(2, 4, 256, 64, 0, 0.0, 0, 0.0, 0, 0, 0)))
+    half = lib.mha_backward_workspace_bytes(C.byref(Cfg(2, 4, 256, 64, 0, 0.0, 0, 0.0, 0, 4, 4)))
+    assert whole > 0 and 0 < half < whole
+    for off, cnt in ((0, 9), (5, 4), (-1, 2), (3, 0), (0, -1)):
+        assert lib.mha_backward_workspace_bytes(C.byref(Cfg(2, 4, 256, 64, 0, 0.0, 0, 0.0, 0, off, cnt))) == 0
+        assert lib.mha_forward_host(C.byref(Cfg(2, 4, 256, 64, 0, 0.0, 0, 0.0, 0, off, cnt)),
+                                    16, 16, 16, 16, 16, None) == 1  # EINVAL
+
+
 def test_cpp_api_header_compiles():
     r = subprocess.run(["bash", "-c", f"echo '#include \"vattn_b200/mha.hpp\"' | g++ -std=c++17 -fsyntax-only "
                                       f"-I{ROOT}/include -I/usr/local/cuda/include -x c++ -"],
@@ -95,4 +110,4 @@ def test_python_mirror_config_validation():
         vb.AttnConfig(seq_len=64, head_dim=64, dropout_p=1.0).validate()
     vb.AttnConfig(seq_len=100, head_dim=64).validate(strict_tiles=False)
     assert abs(vb.AttnConfig(seq_len=64, head_dim=64).scale() - 0.125) < 1e-9
-    assert vb.lib.vattn_abi_version() == 2
+    assert vb.lib.vattn_abi_version() == 3
