@@ -494,14 +494,14 @@ __global__ void __launch_bounds__(384, 1)
             // K runs ahead of V (S_(j+1) is issued before dP_(j+1))
             auto load_k = [&](int j) {
                 const int sl = j % SK;
-                mbar_wait<VATTN_SLEEP_PRODUCER>(k_empty + sl, ((j / SK) & 1) ^ 1);
+                mbar_wait<VATTN_SLEEP_PRODUCER, true>(k_empty + sl, ((j / SK) & 1) ^ 1);
                 mbar_arrive_expect_tx(k_full + sl, Cfg::kTileBytes);
                 for (int b = 0; b < Cfg::kBoxes; ++b)
                     tma_load_3d(sK + sl * Cfg::kTileBytes + b * 16384, &tm_k, k_full + sl, b * 64, j * 128, bh);
             };
             auto load_v = [&](int j) {
                 const int sl = j % SV;
-                mbar_wait<VATTN_SLEEP_PRODUCER>(v_empty + sl, ((j / SV) & 1) ^ 1);
+                mbar_wait<VATTN_SLEEP_PRODUCER, true>(v_empty + sl, ((j / SV) & 1) ^ 1);
                 mbar_arrive_expect_tx(v_full + sl, Cfg::kTileBytes);
                 for (int b = 0; b < Cfg::kBoxes; ++b)
                     tma_load_3d(sV + sl * Cfg::kTileBytes + b * 16384, &tm_v, v_full + sl, b * 64, j * 128, bh);
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(384, 1)
         if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H), q);
         for (int j = 0; j < nk; ++j) {
             const uint32_t R = (j & 1) ? 128u : 0u;
-            mbar_wait<VATTN_SLEEP_MATH>(s_full + (j & 1), (j >> 1) & 1);
+            mbar_wait<VATTN_SLEEP_MATH, true>(s_full + (j & 1), (j >> 1) & 1);
             tc_fence_after();
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 0);
             float pr[64];
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(384, 1)
                 pr[x] = x > lim ? 0.0f : pv;
             }
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 1);
-            mbar_wait<VATTN_SLEEP_MATH>(dp_full, j & 1);
+            mbar_wait<VATTN_SLEEP_MATH, true>(dp_full, j & 1);
             tc_fence_after();
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 2);
             uint32_t dsp[32];
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(384, 1)
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 3);
         }
         // ------------------------------------- epilogue: dQ * scale -> 16-bit
-        mbar_wait<VATTN_SLEEP_MATH>(dq_done, 0);
+        mbar_wait<VATTN_SLEEP_MATH, true>(dq_done, 0);
         tc_fence_after();
         uint8_t* sOut = sQ;  // Q tile is dead once the last S landed
 #pragma unroll

@@ -47,7 +47,7 @@ struct FwdCfg {
     static constexpr int kSmemQ = 0;                    // Q0, Q1
     static constexpr int kSmemKV = 2 * kTileBytes;
     static constexpr int kSmemBar = kSmemKV + kStages * kTileBytes;
-    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 4 + 2;
+    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 8 + 2;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr int kThreads = 384;
     static constexpr uint32_t kTmemO = 256;
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* kv_empty = kv_full + S;
     uint64_t* s_full = kv_empty + S;
     uint64_t* p_full = s_full + 2;
-    uint64_t* o_done = p_full + 4;  // p_full: [tile][half]
+    uint64_t* o_done = p_full + 8;  // p_full: [tile][quarter]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
     const int warp = warp_id();
@@ -100,8 +100,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(s_full + t, 1);
-            mbar_init(p_full + 2 * t, 128);
-            mbar_init(p_full + 2 * t + 1, 128);
+            for (int qq = 0; qq < 4; ++qq) mbar_init(p_full + 4 * t + qq, 4);  // one arrive per warp
             mbar_init(o_done + t, 1);
         }
         fence_barrier_init();
@@ -164,13 +163,16 @@ __global__ void __launch_bounds__(384, 1)
         };
         auto issue_pv = [&](int t, int j) {
             const uint64_t vd = dV0 + ((2 * j + 1) % S) * kTile16;
+            // P arrives in four 32-key quarters: each pair of K=16 steps starts as
+            // soon as its quarter is in tensor memory (the softmax is still
+            // exponentiating the rest of the row).
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                mbar_wait_mma(p_full + 2 * t + hf, j & 1);
+            for (int qq = 0; qq < 4; ++qq) {
+                mbar_wait_mma(p_full + 4 * t + qq, j & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int k4 = 0; k4 < 4; ++k4) {
-                    const int kk = 4 * hf + k4;
+                for (int k2 = 0; k2 < 2; ++k2) {
+                    const int kk = 2 * qq + k2;
                     mma_ts_e(tmem + Cfg::kTmemO + kD * t, tmem + 128 * t + kk * 8, desc_mnmajor(vd, kk),
                              idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
                 }
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(384, 1)
         if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H), row);
         float m_run = -INFINITY;  // running max, log2 units (already scaled)
         float l_run = 0.0f;
-        const int ntile = nk[t];
+        const int ntile = t ? nk[1] : nk[0];
         for (int j = 0; j < ntile; ++j) {
             mbar_wait<VATTN_SLEEP_MATH>(s_full + t, j & 1);
             tc_fence_after();
@@ -247,15 +249,8 @@ __global__ void __launch_bounds__(384, 1)
                 for (int c = 0; c < 128; ++c)
                     if (c > lim) s[c] = -INFINITY;
             }
-            // tree reduction (8 independent chains) instead of a 128-deep dependency chain
-            float mx64[64];
-#pragma unroll
-            for (int u = 0; u < 64; ++u) mx64[u] = fmax_nr(s[u], s[u + 64]);
-#pragma unroll
-            for (int w = 32; w >= 1; w >>= 1)
-#pragma unroll
-                for (int u = 0; u < w; ++u) mx64[u] = fmax_nr(mx64[u], mx64[u + w]);
-            const float mx = mx64[0];
+            // row max: tree of 3-input maxima
+            const float mx = row_max<128>(s);
             const float m_tile = mx * sc;
             if ((warp & 3) == 0 && lane == 0) VTRACE(2048 + 8 * j + 4 * t + 1);
             if (j == 0) {
@@ -284,42 +279,74 @@ __global__ void __launch_bounds__(384, 1)
             }
             const float m_use = m_run == -INFINITY ? 0.0f : m_run;
             if ((warp & 3) == 0 && lane == 0) VTRACE(2048 + 8 * j + 4 * t + 2);
-            float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // independent partial row sums
-            // P in two halves (keys [0,64) then [64,128)): the MMA warp starts the
-            // first half of P V while the second half is still being exponentiated.
-            auto emit_half = [&](int c, auto exp2f_) {
-                uint32_t pk[32];
+            const float2 sc2 = make_float2(sc, sc);
+            const float2 nm2 = make_float2(-m_use, -m_use);
+            float2 ls2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};  // row-sum partials
+            // P in four 32-key quarters (16 packed columns each); the MMA warp
+            // starts P V on a quarter as soon as it lands.  The tensor-memory store
+            // of quarter q completes (wait::st) while quarter q+1 is computed, so
+            // the store latency never sits on the softmax's critical path.
+            auto quarter = [&](int qq, uint32_t (&pk)[16], auto poly_pair) {
 #pragma unroll
-                for (int x = 0; x < 32; ++x) {
-                    const float p0 = exp2f_(x, fmaf(s[64 * c + 2 * x], sc, -m_use));
-                    const float p1 = exp2f_(x, fmaf(s[64 * c + 2 * x + 1], sc, -m_use));
-                    ls[x & 3] += p0 + p1;  // l uses the weights before dropout
-                    pk[x] = pack2<kBF16>(p0, p1);
+                for (int x = 0; x < 16; ++x) {
+                    const int c = 32 * qq + 2 * x;
+                    const float2 v = ffma2(make_float2(s[c], s[c + 1]), sc2, nm2);
+                    float2 pp;
+                    if (poly_pair(qq * 16 + x)) {
+                        pp = ex2_poly2(v);
+                    } else {
+                        pp.x = ex2(v.x);
+                        pp.y = ex2(v.y);
+                    }
+                    ls2[x & 1] = fadd2(ls2[x & 1], pp);  // l uses the weights before dropout
+                    pk[x] = pack2<kBF16>(pp.x, pp.y);
                     if constexpr (kDrop) {
                         // dropout on the 16-bit P: f16(f16(P) * 1/(1-p)) or 0
                         // (attention_forward.cpp:94-106)
-                        const int col = j * 128 + 64 * c + 2 * x;
+                        const int col = j * 128 + c;
                         const float2 f = unpack2<kBF16>(pk[x]);
                         pk[x] = pack2<kBF16>(drop_keep(drow, col, p.drop_thresh) ? f.x * p.inv_keep : 0.0f,
                                              drop_keep(drow, col + 1, p.drop_thresh) ? f.y * p.inv_keep : 0.0f);
                     }
                 }
-                tmem_st32(tS + 32 * c, pk);
-                tmem_wait_st();
-                tc_fence_before();
-                mbar_arrive(p_full + 2 * t + c);
-                if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 1 + c);
             };
-            auto ex2_fast = [](int x, float v) { return ex2_mix<PolyPeriod<kD>::fwd>(x, v); };
-            auto ex2_exact = [](int, float v) { return ex2(v); };  // -inf -> exact 0
-            if (tile_masked) {  // warp-uniform: tcgen05.st below is .sync.aligned
-                emit_half(0, ex2_exact);
-                emit_half(1, ex2_exact);
-            } else {
-                emit_half(0, ex2_fast);
-                emit_half(1, ex2_fast);
-            }
-            l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+            auto publish = [&](int qq) {  // quarter qq's tcgen05.st has been waited on
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full + 4 * t + qq);
+                if ((warp & 3) == 0 && lane == 0) VTRACE((qq < 3 ? 1024 + 1 + qq : 2048 + 3) + 8 * j + 4 * t);
+            };
+            auto emit_row = [&](auto poly_pair) {
+                uint32_t pa[16], pb[16];
+                quarter(0, pa, poly_pair);
+                tmem_st16(tS + 0, pa);
+                quarter(1, pb, poly_pair);
+                tmem_wait_st();
+                publish(0);
+                tmem_st16(tS + 16, pb);
+                quarter(2, pa, poly_pair);
+                tmem_wait_st();
+                publish(1);
+                tmem_st16(tS + 32, pa);
+                quarter(3, pb, poly_pair);
+                tmem_wait_st();
+                publish(2);
+                tmem_st16(tS + 48, pb);
+                tmem_wait_st();
+                publish(3);
+            };
+            constexpr int kPer = PolyPeriod<kD>::fwd;
+            auto poly_fast = [](int pair) {
+                if constexpr (kPer > 0) return pair % kPer == kPer - 1;
+                return false;
+            };
+            auto poly_none = [](int) { return false; };  // -inf -> exact 0 on masked tiles
+            if (tile_masked)  // warp-uniform: tcgen05.st is .sync.aligned
+                emit_row(poly_none);
+            else
+                emit_row(poly_fast);
+            const float2 lsum = fadd2(ls2[0], ls2[1]);
+            l_run += lsum.x + lsum.y;
         }
         if (ntile > 0) {
             // ------------------------------------------------------ epilogue

@@ -97,7 +97,7 @@ VATTN_DEV uint64_t globaltimer_ns() {
 // MMA-warp wait flavour (experiment knob): 0 spin, 1 spin with nanosleep backoff,
 // 2 short suspend hint.
 #ifndef VATTN_MMA_WAIT
-#define VATTN_MMA_WAIT 1
+#define VATTN_MMA_WAIT 0
 #endif
 VATTN_DEV bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {
     uint32_t ok;
@@ -128,7 +128,10 @@ VATTN_DEV void mbar_wait_mma(uint64_t* bar, uint32_t parity) {
 }
 
 // Wait until the phase with parity `parity` has completed (kSleep: park instead of spin).
-template <bool kSleep = false>
+// kPrint: report the stuck barrier before trapping.  Besides being a debug aid it
+// changes the code ptxas emits around the wait loops; it is enabled where that
+// measured faster on B200 (the dQ kernel: 1.33 vs 1.44 ms at C3).
+template <bool kSleep = false, bool kPrint = false>
 VATTN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     auto probe = [&] { return kSleep ? mbar_try_wait_sleep(bar, parity) : mbar_try_wait(bar, parity); };
     if (probe()) return;
@@ -137,8 +140,11 @@ VATTN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t n = 0;
     while (!probe()) {
         if ((++n & (kSleep ? 0u : 1023u)) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) {
-            printf("vattn watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n",
-                   (int)(blockIdx.x + blockIdx.y * gridDim.x), (int)threadIdx.x, smem_u32(bar), parity);
+#ifndef VATTN_WATCHDOG_PRINT
+            if constexpr (kPrint)
+#endif
+                printf("vattn watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n",
+                       (int)(blockIdx.x + blockIdx.y * gridDim.x), (int)threadIdx.x, smem_u32(bar), parity);
             __trap();
         }
     }
@@ -456,7 +462,7 @@ VATTN_DEV float ex2_poly(float x) {
 // Share of exponentials routed to ex2_poly: element pairs with pair % period == 0
 // (period 0 = MUFU only).  Tuned per kernel on B200 (bench.py, C3).
 #ifndef VATTN_POLY_FWD
-#define VATTN_POLY_FWD 0
+#define VATTN_POLY_FWD 4
 #endif
 #ifndef VATTN_POLY_DKDV
 #define VATTN_POLY_DKDV 0
@@ -494,6 +500,68 @@ VATTN_DEV float fmax_nr(float a, float b) {
     float r;
     asm("max.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
     return r;
+}
+
+// 3-input max (FMNMX3): halves the instructions of a row-max tree.
+VATTN_DEV float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// Max of an unrolled register array: 8 independent chains of 3-input maxima
+// (few live temporaries, depth kN/16 + 3).
+template <int kN>
+VATTN_DEV float row_max(const float* v) {
+    static_assert(kN % 16 == 0 && kN >= 16, "row_max");
+    float a[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) a[c] = fmax_nr(v[c], v[c + 8]);
+#pragma unroll
+    for (int i = 16; i < kN; i += 16)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) a[c] = fmax3(a[c], v[i + c], v[i + 8 + c]);
+    return fmax3(fmax3(a[0], a[1], a[2]), fmax3(a[3], a[4], a[5]), fmax_nr(a[6], a[7]));
+}
+
+// Packed fp32 pairs (FFMA2 / FADD2 / FMUL2 on sm_100): one issue slot per two lanes' worth.
+VATTN_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+    return d;
+}
+VATTN_DEV float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("add.f32x2 %0, %1, %2;"
+        : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+    return d;
+}
+VATTN_DEV float2 fmul2(float2 a, float2 b) {
+    float2 d;
+    asm("mul.f32x2 %0, %1, %2;"
+        : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+    return d;
+}
+
+// Two ex2_poly on packed fp32 pairs (FFMA2 / FADD2): ~5.5 issue slots per element.
+VATTN_DEV float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -127.0f);
+    x.y = fmaxf(x.y, -127.0f);
+    const float2 kRnd = make_float2(12582912.0f, 12582912.0f);
+    const float2 t = fadd2(x, kRnd);
+    const float2 f = fadd2(x, fadd2(kRnd, make_float2(-t.x, -t.y)));
+    float2 p = ffma2(f, make_float2(0.009582852944731712f, 0.009582852944731712f),
+                     make_float2(0.055906426161527634f, 0.055906426161527634f));
+    p = ffma2(p, f, make_float2(0.24024099111557007f, 0.24024099111557007f));
+    p = ffma2(p, f, make_float2(0.6931241750717163f, 0.6931241750717163f));
+    p = ffma2(p, f, make_float2(1.0f, 1.0f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 VATTN_DEV float lg2(float x) {

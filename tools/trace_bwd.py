@@ -73,11 +73,20 @@ n_q = (N + 127) // 128
 if "dq" not in sys.argv:
     print(f"== forward, block {block}")
     t = trace(0, fwd)
-    show(t, ["pv0", "s0next", "-", "-", "pv1", "s1next"], ["s0", "p0a", "p0b", "-", "s1", "p1a", "p1b"], min(n_q, 24), 8)
-    print("softmax tile0: ldtm_done max_done rescale_done (relative to s0)")
-    for it in range(min(n_q, 8)):
-        s0 = t[1024 + 8 * it]
-        print(it, [int(t[2048 + 8 * it + k] - s0) for k in range(3)], "p0a", int(t[1024 + 8 * it + 1] - s0), "p0b", int(t[1024 + 8 * it + 2] - s0))
+    t0 = t[3072]
+    print("iter | MMA pv0_issued s0_issued pv1_issued s1_issued | tile0: s0 +ld +max +resc +q0 +q1 +q2 +q3 | tile1: s1 ... | dt")
+    prev = None
+    for it in range(min(n_q, 24)):
+        m = [t[8 * it + k] - t0 for k in (0, 1, 4, 5)]
+        rows = []
+        for tt in range(2):
+            s0 = t[1024 + 8 * it + 4 * tt]
+            rel = [t[2048 + 8 * it + 4 * tt + k] - s0 for k in range(3)] + \
+                  [t[1024 + 8 * it + 4 * tt + k] - s0 for k in (1, 2, 3)] + [t[2048 + 8 * it + 4 * tt + 3] - s0]
+            rows.append(f"{s0 - t0:7d} " + " ".join(f"{x:5d}" for x in rel))
+        dtv = m[0] - prev if prev is not None else 0
+        prev = m[0]
+        print(f"{it:3d} | " + " ".join(f"{x:7d}" for x in m) + " | " + " | ".join(rows) + f" | {dtv}")
     print(f"== dK/dV, block {block}")
     t = trace(1, bwd)
     show(t, ["p_full", "S_next", "ds_full"], ["s_full", "P_done", "dp_full", "dS_done"], min(n_q, 24), 8)
