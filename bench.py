@@ -42,8 +42,14 @@ METRIC = "MHA fwd+bwd TFLOPS and % of B200 tensor peak at 1/2/4/8 GPUs vs CPU re
 CONFIGS = {
     # name: (B, H, N, d, causal, dtype, description)
     "c3": (4, 16, 8192, 128, True, "bf16", "BASELINE configs[2]: causal MHA fwd+bwd, d=128, B=4, H=16, N=8192, bf16"),
+    "c2_512": (32, 32, 512, 64, False, "fp16", "BASELINE configs[1] point: 16k tokens, hidden 2048, d=64, N=512"),
+    "c2_1k": (16, 32, 1024, 64, False, "fp16", "BASELINE configs[1] point: 16k tokens, hidden 2048, d=64, N=1024"),
+    "c2_2k": (8, 32, 2048, 64, False, "fp16", "BASELINE configs[1] point: 16k tokens, hidden 2048, d=64, N=2048"),
     "c2_4k": (4, 32, 4096, 64, False, "fp16", "BASELINE configs[1] point: 16k tokens, hidden 2048, d=64, N=4096"),
+    "c2_8k": (2, 32, 8192, 64, False, "fp16", "BASELINE configs[1] point: 16k tokens, hidden 2048, d=64, N=8192"),
     "c2_16k": (1, 32, 16384, 64, False, "fp16", "BASELINE configs[1] point: 16k tokens, hidden 2048, d=64, N=16384"),
+    "c3_fp16": (4, 16, 8192, 128, True, "fp16", "BASELINE configs[2] in fp16: causal MHA fwd+bwd, d=128, B=4, H=16, N=8192"),
+    "c3_nc": (4, 16, 8192, 128, False, "bf16", "BASELINE configs[2] shape, non-causal: d=128, B=4, H=16, N=8192, bf16"),
     "c4": (8, 16, 1024, 64, True, "fp16", "BASELINE configs[3] per layer: GPT-2-medium attention, causal"),
     "c5": (1, 64, 32768, 128, True, "bf16", "BASELINE configs[4] on one GPU: causal seq 32k, d=128, H=64"),
 }

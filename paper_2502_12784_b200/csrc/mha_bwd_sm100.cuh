@@ -126,9 +126,9 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* q_empty = q_full + kSt;     // [kSt]
     uint64_t* s_full = q_empty + kSt;
     uint64_t* dp_full = s_full + 1;
-    uint64_t* p_full = dp_full + 1;
-    uint64_t* ds_full = p_full + 1;
-    uint64_t* dkv_full = ds_full + 1;
+    uint64_t* p_full = dp_full + 1;   // [warpgroup]
+    uint64_t* ds_full = p_full + 2;   // [warpgroup]
+    uint64_t* dkv_full = ds_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
     const int warp = warp_id();
@@ -149,8 +149,10 @@ __global__ void __launch_bounds__(384, 1)
         }
         mbar_init(s_full, 1);
         mbar_init(dp_full, 1);
-        mbar_init(p_full, 8);
-        mbar_init(ds_full, 8);
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(p_full + x, 4);  // one arrive per warp of warpgroup x
+            mbar_init(ds_full + x, 4);
+        }
         mbar_init(dkv_full, 1);
         fence_barrier_init();
     }
@@ -205,11 +207,17 @@ __global__ void __launch_bounds__(384, 1)
         };
         // A operand (16-bit) held in TMEM by the two warpgroups: queries
         // [64h, 64h+64) at columns base + 64h + [0, 32).
-        auto issue_ts = [&](uint32_t dcol, uint32_t abase_col, uint64_t bd, bool acc) {
+        // Warpgroup h's four K-steps are issued as soon as h published (`ready[h]`).
+        auto issue_ts = [&](uint32_t dcol, uint32_t abase_col, uint64_t bd, bool acc, uint64_t* ready, uint32_t ph) {
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
+            for (int kk = 0; kk < 8; ++kk) {
+                if ((kk & 3) == 0) {
+                    mbar_wait_mma(ready + (kk >> 2), ph);
+                    tc_fence_after();
+                }
                 mma_ts_e(tmem + dcol, tmem + abase_col + (kk >> 2) * 64 + (kk & 3) * 8, desc_mnmajor(bd, kk),
                          idesc_kmn, (acc || kk > 0) ? 1u : 0u);
+            }
         };
         mbar_wait(kv_full, 0);
         tc_fence_after();
@@ -223,10 +231,8 @@ __global__ void __launch_bounds__(384, 1)
         for (int s = 0; s < n_steps; ++s) {
             const int st = s % kSt;
             const int st1 = (s + 1) % kSt;
-            mbar_wait(p_full, s & 1);
-            tc_fence_after();
+            issue_ts(Cfg::kTmemDV, Cfg::kTmemS, dDOm + st * kTile16, s > 0, p_full, s & 1);  // dV += P^T dO
             VTRACE(8 * s + 0);
-            issue_ts(Cfg::kTmemDV, Cfg::kTmemS, dDOm + st * kTile16, s > 0);  // dV += P^T dO
             if (s + 1 < n_steps) {
                 mbar_wait(q_full + st1, ((s + 1) / kSt) & 1);
                 tc_fence_after();
@@ -234,10 +240,8 @@ __global__ void __launch_bounds__(384, 1)
                 issue_kk(Cfg::kTmemS, dK, dQk + st1 * kTile16);  // in-order after dV read P^T
                 mma_commit_e(s_full);
             }
-            mbar_wait(ds_full, s & 1);
-            tc_fence_after();
+            issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, s & 1);  // dK += dS^T Q
             VTRACE(8 * s + 2);
-            issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0);  // dK += dS^T Q
             mma_commit_e(q_empty + st);
             if (s + 1 < n_steps) {
                 issue_kk(Cfg::kTmemDP, dV, dDOk + st1 * kTile16);  // after dK read dS^T
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(384, 1)
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(p_full);
+            if (lane == 0) mbar_arrive(p_full + h);
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 1);
 
             mbar_wait(dp_full, s & 1);
@@ -347,7 +351,7 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(ds_full);
+                mbar_arrive(ds_full + h);
                 mbar_arrive(q_empty + st);  // done with lse2 / D of this stage
             }
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 3);
