@@ -110,7 +110,14 @@ VATTN_DEV bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {
         : "memory");
     return ok != 0;
 }
+// Whole-warp wait of an MMA-issuing warp: the lanes may leave the polling loop at
+// different iterations, so they are re-converged before the caller's elect.sync.
+VATTN_DEV void mbar_wait_mma_(uint64_t* bar, uint32_t parity);
 VATTN_DEV void mbar_wait_mma(uint64_t* bar, uint32_t parity) {
+    mbar_wait_mma_(bar, parity);
+    __syncwarp();
+}
+VATTN_DEV void mbar_wait_mma_(uint64_t* bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = globaltimer_ns();
     uint32_t n = 0;
