@@ -12,8 +12,8 @@ LIB = os.path.join(ROOT, "paper_2502_12784_b200", "libvattn_b200.so")
 HEADER = os.path.join(ROOT, "include", "vattn_b200.h")
 
 
-def declared_functions():
-    src = open(HEADER).read()
+def declared_functions(header=HEADER):
+    src = open(header).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_]+\s*\*?\s*([a-z_0-9]+)\s*\(", src, flags=re.M)))
 
@@ -32,11 +32,22 @@ def test_header_declares_the_boundary():
         assert f in fns, fns
 
 
-def test_library_exports_every_declared_symbol(lib):
-    nm = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True, check=True).stdout
+TRAD_LIB = os.path.join(ROOT, "paper_2502_12784_b200", "libvattn_b200_traditional.so")
+TRAD_HEADER = os.path.join(ROOT, "include", "vattn_b200_traditional.h")
+
+
+@pytest.mark.parametrize("lib_path,header", [(LIB, HEADER), (TRAD_LIB, TRAD_HEADER)])
+def test_library_exports_every_declared_symbol(lib, lib_path, header):
+    nm = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True, check=True).stdout
     exported = set(re.findall(r" T (\w+)$", nm, flags=re.M))
-    missing = [f for f in declared_functions() if f not in exported]
-    assert not missing, missing
+    missing = [f for f in declared_functions(header) if f not in exported]
+    assert declared_functions(header) and not missing, missing
+
+
+def test_fused_library_does_not_link_cublas():
+    """The hot path is hand-written; only the comparator library links cuBLAS."""
+    ldd = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout
+    assert "cublas" not in ldd, ldd
 
 
 def test_sm100a_code_only():

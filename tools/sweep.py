@@ -87,6 +87,37 @@ def run_one(name, B, H, N, d, causal, dtype, steps):
                 bwd_tflops=fb / (ms - fwd) / 1e9, dkdv_ms=dkdv, dq_ms=dqk)
 
 
+def run_traditional(name, B, H, N, d, causal, dtype, steps):
+    """The unfused three-pass forward (comparator) vs the fused forward."""
+    from paper_2502_12784_b200 import traditional as tr
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    q, k, v = (torch.randn((B, H, N, d), generator=g, device="cuda").to(dtype) for _ in range(3))
+    ws = torch.empty(tr.workspace_bytes(q, causal), dtype=torch.uint8, device="cuda")
+    o = torch.empty_like(q)
+    lse = torch.empty((B, H, N), device="cuda")
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / steps
+
+    t_trad = timeit(lambda: tr.forward_traditional(q, k, v, causal, workspace=ws))
+    t_fused = timeit(lambda: vb.mha_forward(q, k, v, causal, out=o, lse=lse))
+    ff, _ = flops(B, H, N, d, causal)
+    return dict(config=f"{name} forward: traditional vs fused", shape=[B, H, N, d], causal=causal,
+                dtype=str(dtype).split(".")[-1], traditional_ms=t_trad, fused_ms=t_fused,
+                speedup=t_trad / t_fused, traditional_tflops=ff / t_trad / 1e9, fused_tflops=ff / t_fused / 1e9,
+                traditional_workspace_gb=ws.numel() / 1e9)
+
+
 def run_c4(steps, layers=24):
     B, H, N, d, causal, dtype = 8, 16, 1024, 64, True, torch.float16
     g = torch.Generator(device="cuda")
@@ -150,11 +181,16 @@ def main():
     r = run_c4(args.steps)
     rows.append(r)
     print(json.dumps(r), flush=True)
+    trad = []
+    for cfg in [c for c in CONFIGS if c[0] in ("C2 N=1k", "C2 N=4k", "C3", "C3 non-causal")]:
+        t = run_traditional(*cfg, steps=max(2, args.steps // 2))
+        trad.append(t)
+        print(json.dumps(t), flush=True)
     name = torch.cuda.get_device_name()
     os.makedirs(args.out, exist_ok=True)
     with open(os.path.join(args.out, f"{args.tag}_sweep.json"), "w") as f:
         json.dump({"gpu": name, "peak_bf16_tflops": {"burst": burst, "sustained": sust, "source": src},
-                   "rows": rows}, f, indent=1)
+                   "rows": rows, "traditional_vs_fused": trad}, f, indent=1)
     with open(os.path.join(args.out, f"{args.tag}_sweep.md"), "w") as f:
         f.write(f"# {args.tag} throughput sweep over BASELINE.json configs ({name}, 1 GPU)\n\n")
         f.write("`python tools/sweep.py` -- CUDA events, 3 warm-up steps; TFLOPS = algorithmic "
@@ -169,6 +205,15 @@ def main():
         c4 = rows[-1]
         f.write(f"\nC4 eager (no graph): {c4['eager_ms']:.3f} ms per 24-layer step = {c4['eager_tflops']:.0f} TFLOPS; "
                 f"graph replay {c4['ms']:.3f} ms = {c4['tflops']:.0f} TFLOPS ({c4['launches_per_step']} kernels).\n")
+        f.write("\n## Fused vs traditional forward (the paper's comparison, SURVEY 8f-3)\n\n"
+                "Traditional = `mha_forward_traditional` (S = QK^T in binary32 via cuBLAS, full-row softmax "
+                "kernel, O = PV via cuBLAS; every key tile computed and masked, as the reference's "
+                "`forward_traditional`).  TFLOPS use the same algorithmic count for both.\n\n"
+                "| config | traditional ms | fused ms | speedup | traditional TFLOPS | fused TFLOPS | S+P workspace GB |\n"
+                "|---|---|---|---|---|---|---|\n")
+        for t in trad:
+            f.write(f"| {t['config']} | {t['traditional_ms']:.3f} | {t['fused_ms']:.3f} | {t['speedup']:.1f}x | "
+                    f"{t['traditional_tflops']:.0f} | {t['fused_tflops']:.0f} | {t['traditional_workspace_gb']:.1f} |\n")
 
 
 if __name__ == "__main__":
