@@ -73,14 +73,69 @@ struct AttnConfig {
     size_t rows() const { return static_cast<size_t>(batch) * heads * seq_len; }
 };
 
+// vattn::TrafficCounter (include/vattn/traffic.hpp:12-31).  The GPU path emulates
+// nothing, so the reference's modeled-HBM counters are filled from closed forms of
+// its own bookkeeping (traffic_* below; pinned to the reference library by
+// tests/test_traffic_spat.py and tests/cpp/mha_cpp_parity.cpp).  The Volta
+// datapath events (mma_invocations, shuffle_events, convert_events) have no B200
+// counterpart and stay 0; measured DRAM bytes are in profiles/.
+struct TrafficCounter {
+    uint64_t matrix_pass_reads = 0;
+    uint64_t matrix_pass_writes = 0;
+    uint64_t element_reads = 0;
+    uint64_t element_writes = 0;
+    uint64_t mma_invocations = 0;
+    uint64_t shuffle_events = 0;
+    uint64_t convert_events = 0;
+};
+
 struct ForwardOutput {
     std::vector<uint16_t> out;  // [B, H, N, d] 16-bit bit patterns
     std::vector<float> lse;     // [B, H, N]
+    TrafficCounter traffic;     // closed forms of attention.hpp:40-50
+    uint64_t mask_digest = 0;   // tiling-dependent reference test hook: not produced
 };
 
 struct GradOutputs {
     std::vector<uint16_t> dq, dk, dv;  // [B, H, N, d]
+    TrafficCounter traffic;            // closed forms of attention_backward.cpp:59-219
+    uint64_t mask_digest = 0;
 };
+
+// (query-tile, key-tile) pairs a reference fused pass visits per (b, h)
+// (causal: key tile kt is visited by query tile qt iff kt*Bc <= qt*Br + Br - 1,
+// attention_forward.cpp:128, attention_backward.cpp:125).
+inline uint64_t visited_pairs(const AttnConfig& c) {
+    const int nq = c.seq_len / c.tile_rows, nk = c.seq_len / c.tile_cols;
+    if (!c.causal) return static_cast<uint64_t>(nq) * nk;
+    uint64_t t = 0;
+    for (int qt = 0; qt < nq; ++qt) {
+        const int last = (qt * c.tile_rows + c.tile_rows - 1) / c.tile_cols + 1;
+        t += static_cast<uint64_t>(last < nk ? last : nk);
+    }
+    return t;
+}
+
+inline TrafficCounter traffic_forward_fused(const AttnConfig& c) {
+    const uint64_t BH = static_cast<uint64_t>(c.batch) * c.heads, N = c.seq_len, d = c.head_dim;
+    TrafficCounter t;
+    t.matrix_pass_reads = 3;  // Q, K, V
+    t.matrix_pass_writes = 1;  // O
+    t.element_reads = BH * (N * d + 2ull * c.tile_cols * d * visited_pairs(c));
+    t.element_writes = BH * (N * d + N);
+    return t;
+}
+
+inline TrafficCounter traffic_backward_fused(const AttnConfig& c) {
+    const uint64_t BH = static_cast<uint64_t>(c.batch) * c.heads, N = c.seq_len, d = c.head_dim;
+    const uint64_t br = c.tile_rows, bc = c.tile_cols, T = visited_pairs(c), nk = N / bc;
+    TrafficCounter t;
+    t.matrix_pass_reads = 10;  // pre-pass Q K V; Q K V dO lse D; dQ finalize read
+    t.matrix_pass_writes = 5;  // D, dK, dV, dQ adds, dQ narrowing
+    t.element_reads = BH * ((N * d + 2 * bc * d * T) + 2 * bc * d * nk + T * (2 * br * d + 2 * br) + N * d);
+    t.element_writes = BH * (N + T * br * d + 2 * bc * d * nk + N * d);
+    return t;
+}
 
 namespace detail {
 
@@ -179,6 +234,7 @@ inline ForwardOutput forward_fused(const std::vector<uint16_t>& q, const std::ve
     ForwardOutput r;
     r.out.resize(cfg.elems());
     r.lse.resize(rows);
+    r.traffic = traffic_forward_fused(cfg);
     const vattn_config c = detail::to_c(cfg, dn);
     if (dn == cfg.head_dim) {
         detail::check(mha_forward_host(&c, q.data(), k.data(), v.data(), r.out.data(), r.lse.data(), nullptr),
@@ -227,6 +283,7 @@ inline GradOutputs backward_fused(const std::vector<uint16_t>& q, const std::vec
                                bdq.p, bdk.p, bdv.p, ws.p, wsb, s),
                   "mha_backward");
     GradOutputs g;
+    g.traffic = traffic_backward_fused(cfg);
     g.dq.resize(cfg.elems());
     g.dk.resize(cfg.elems());
     g.dv.resize(cfg.elems());

@@ -96,6 +96,10 @@ def ref_lib():
         lib.vr_attention_grad_ref_dropout.argtypes = [_i32] * 5 + [_f32, _f32, _u64] + [_f64p] * 7
         lib.vr_bench_units.argtypes = [_i32] * 5
         lib.vr_bench_units.restype = C.c_double
+        lib.vr_traffic.argtypes = [_i32] * 8 + [_u64p]
+        lib.vr_write_spat_f16.argtypes = [C.c_char_p, _i32, _u64p, _u16p]
+        lib.vr_write_spat_f32.argtypes = [C.c_char_p, _i32, _u64p, _f32p]
+        lib.vr_read_spat_check.argtypes = [C.c_char_p]
         _ref = lib
     return _ref
 

@@ -30,6 +30,7 @@
 #include "vattn/attention.hpp"
 #include "vattn/backward.hpp"
 #include "vattn/reference.hpp"
+#include "vattn/tensor_io.hpp"
 #include "vattn/workload.hpp"
 
 using namespace vattn;
@@ -278,6 +279,57 @@ double vr_bench_units(int N, int d, int causal, int units, int threads) {
     const double secs =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return failed.load() ? -1.0 : secs;
+}
+
+// ---- TrafficCounter of the reference's own passes (pins the closed forms in
+// paper_2502_12784_b200/traffic.py).  out[7] = matrix_pass_reads, matrix_pass_writes,
+// element_reads, element_writes, mma_invocations, shuffle_events, convert_events.
+static void put_traffic(const TrafficCounter& t, uint64_t* out) {
+    out[0] = t.matrix_pass_reads;
+    out[1] = t.matrix_pass_writes;
+    out[2] = t.element_reads;
+    out[3] = t.element_writes;
+    out[4] = t.mma_invocations;
+    out[5] = t.shuffle_events;
+    out[6] = t.convert_events;
+}
+
+int vr_traffic(int which, int B, int H, int N, int d, int br, int bc, int causal, uint64_t* out) {
+    return guarded([&] {
+        const auto dims = dims4(B, H, N, d);
+        const Tensor<Half> q = normal_tensor_f16(1, 1, dims), k = normal_tensor_f16(1, 2, dims),
+                           v = normal_tensor_f16(1, 3, dims), dout = normal_tensor_f16(1, 4, dims);
+        if (which == 0) {  // forward_fused, FP32-ACC
+            put_traffic(forward_fused(q, k, v, make_cfg(B, H, N, d, br, bc, causal, 0, 0.0f)).traffic, out);
+        } else if (which == 1) {  // forward_traditional, FP32-ACC
+            put_traffic(forward_traditional(q, k, v, make_cfg(B, H, N, d, br, bc, causal, 0, 0.0f)).traffic, out);
+        } else {  // backward_fused (FP16-ACC, its only mode)
+            const AttnConfig c = make_cfg(B, H, N, d, br, bc, causal, 1, 0.0f);
+            const ForwardOutput f = forward_fused(q, k, v, c);
+            put_traffic(backward_fused(q, k, v, dout, f.lse, c).traffic, out);
+        }
+    });
+}
+
+// ---- SPAT container round trips through the reference's tensor_io.cpp
+int vr_write_spat_f16(const char* path, int rank, const uint64_t* dims, const uint16_t* bits) {
+    return guarded([&] {
+        std::vector<std::size_t> dv(dims, dims + rank);
+        Tensor<Half> t(dv);
+        for (std::size_t i = 0; i < t.size(); ++i) t.data()[i] = Half::from_bits(bits[i]);
+        write_spat(path, t);
+    });
+}
+int vr_write_spat_f32(const char* path, int rank, const uint64_t* dims, const float* vals) {
+    return guarded([&] {
+        std::vector<std::size_t> dv(dims, dims + rank);
+        Tensor<float> t(dv);
+        std::memcpy(t.data(), vals, t.size() * sizeof(float));
+        write_spat(path, t);
+    });
+}
+int vr_read_spat_check(const char* path) {  // 0 = reads cleanly, else the error class
+    return guarded([&] { (void)read_spat(path); });
 }
 
 }  // extern "C"

@@ -62,6 +62,11 @@ static void run_case(int B, int H, int N, int d, bool causal, uint64_t seed) {
                             " d" + std::to_string(d) + (causal ? " causal" : "");
     const auto o = widen_bits(ours.out, dims);
     check(close(o, ref.out, 1e-3, 2e-3, "O vs binary64"), tag + ": O vs attention_ref");
+    check(ours.traffic.matrix_pass_reads == fused.traffic.matrix_pass_reads &&
+              ours.traffic.matrix_pass_writes == fused.traffic.matrix_pass_writes &&
+              ours.traffic.element_reads == fused.traffic.element_reads &&
+              ours.traffic.element_writes == fused.traffic.element_writes,
+          tag + ": TrafficCounter closed forms == forward_fused's counters");
     check(close(o, vattn::widen(fused.out), 1e-3, 2e-3, "O vs forward_fused"), tag + ": O vs forward_fused FP32-ACC");
     double lse_rel = 0;
     for (size_t i = 0; i < ours.lse.size(); ++i)
