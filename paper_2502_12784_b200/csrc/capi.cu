@@ -190,7 +190,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     p.causal = c->causal;
     p.scale_log2 = eff_scale(c) * kLog2e;
     set_dropout(c, &p.H, &p.bh_off, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
-    dim3 grid((N + 255) / 256, BH);
+    const dim3 grid = tile_grid((N + 255) / 256, BH);
     {
         ProfScope prof(stream, 0);
         kern<<<grid, FwdCfg<kD>::kThreads, smem, stream>>>(mq, mk, mv, mo, p);
@@ -270,7 +270,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
-        kern<<<dim3(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, dk, dv, p);
+        kern<<<tile_grid(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, dk, dv, p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)
     {
@@ -279,7 +279,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const cudaError_t ae = set_smem_once<mha_bwd_dq_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 2);
-        kern<<<dim3(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, mdq, p);
+        kern<<<tile_grid(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, mdq, p);
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("mha_bwd launch: ") + cudaGetErrorString(e));

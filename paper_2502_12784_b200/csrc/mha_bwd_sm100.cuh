@@ -25,34 +25,46 @@ namespace vattn_sm100 {
 // ------------------------------------------------------------ preprocess --
 
 // D = rowsum(dO o O) (compute_dpsum), lse2 = lse * log2(e); both padded to Npad
-// (+inf / 0) so 128-row tiles never read past a head.  One warp per row.
+// (+inf / 0) so 128-row tiles never read past a head.  HBM-bound: every thread
+// loads 16 bytes of O and of dO per row (kD / 8 threads per row, so a warp covers
+// 32 * 8 / kD contiguous rows), products summed in fp32 and reduced over the row's
+// lanes with shuffles.
 template <int kD, bool kBF16>
 __global__ void __launch_bounds__(256) mha_bwd_preprocess_kernel(
     const void* __restrict__ o, const void* __restrict__ dout, const float* __restrict__ lse,
     float* __restrict__ lse2, float* __restrict__ dsum, int N, int Npad, int BH) {
     using T16 = typename std::conditional<kBF16, __nv_bfloat16, __half>::type;
+    constexpr int kLanesPerRow = kD / 8;
+    constexpr int kRowsPerWarp = 32 / kLanesPerRow;
     const int lane = threadIdx.x & 31;
+    const int sub = lane % kLanesPerRow;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (int row = gw; row < BH * Npad; row += nwarps) {
-        const int bh = row / Npad;
-        const int n = row - bh * Npad;
+    const long long rows = static_cast<long long>(BH) * Npad;
+    for (long long r0 = static_cast<long long>(gw) * kRowsPerWarp; r0 < rows;
+         r0 += static_cast<long long>(nwarps) * kRowsPerWarp) {
+        const long long row = r0 + lane / kLanesPerRow;
+        const int bh = static_cast<int>(row / Npad);
+        const int n = static_cast<int>(row - static_cast<long long>(bh) * Npad);
+        const bool valid = row < rows && n < N;
         float acc = 0.0f;
-        float l2 = INFINITY;
-        if (n < N) {
-            const size_t base = (static_cast<size_t>(bh) * N + n) * kD;
-            constexpr int kPer = kD / 32;
-            const T16* po = reinterpret_cast<const T16*>(o) + base + lane * kPer;
-            const T16* pd = reinterpret_cast<const T16*>(dout) + base + lane * kPer;
+        if (valid) {
+            const size_t base = (static_cast<size_t>(bh) * N + n) * kD + sub * 8;
+            const uint4 a = *reinterpret_cast<const uint4*>(reinterpret_cast<const T16*>(o) + base);
+            const uint4 g = *reinterpret_cast<const uint4*>(reinterpret_cast<const T16*>(dout) + base);
+            const uint32_t av[4] = {a.x, a.y, a.z, a.w}, gv[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
-            for (int e = 0; e < kPer; ++e) acc += static_cast<float>(pd[e]) * static_cast<float>(po[e]);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            l2 = lse[static_cast<size_t>(bh) * N + n] * 1.4426950408889634f;
+            for (int e = 0; e < 4; ++e) {
+                const float2 x = unpack2<kBF16>(av[e]), y = unpack2<kBF16>(gv[e]);
+                acc = fmaf(y.x, x.x, acc);
+                acc = fmaf(y.y, x.y, acc);
+            }
         }
-        if (lane == 0) {
-            dsum[row] = n < N ? acc : 0.0f;
-            lse2[row] = l2;
+#pragma unroll
+        for (int off = kLanesPerRow / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (sub == 0 && row < rows) {
+            dsum[row] = valid ? acc : 0.0f;
+            lse2[row] = valid ? lse[static_cast<size_t>(bh) * N + n] * 1.4426950408889634f : INFINITY;
         }
     }
 }
@@ -133,9 +145,9 @@ __global__ void __launch_bounds__(384, 1)
 
     const int warp = warp_id();
     const int lane = lane_id();
-    const int bh = blockIdx.y;
+    const int bh = grid_bh();
     // causal: the key tiles with the most query tiles first
-    const int kb = static_cast<int>(blockIdx.x);
+    const int kb = grid_tile();
     const int N = p.N;
     const int i0 = p.causal ? kb : 0;
     const int n_steps = p.n_q - i0;
@@ -451,9 +463,9 @@ __global__ void __launch_bounds__(384, 1)
 
     const int warp = warp_id();
     const int lane = lane_id();
-    const int bh = blockIdx.y;
-    const int nqb = gridDim.x;
-    const int i = p.causal ? (nqb - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
+    const int bh = grid_bh();
+    const int nqb = grid_ntiles();
+    const int i = p.causal ? (nqb - 1 - grid_tile()) : grid_tile();
     const int N = p.N;
     const int nk = p.causal ? i + 1 : p.n_q;
 
@@ -613,9 +625,12 @@ __global__ void __launch_bounds__(384, 1)
             if (p.causal && j == i) lim = min(lim, q - kbase);
             lim = min(lim, N - 1 - kbase);
 #pragma unroll
-            for (int x = 0; x < 64; ++x) {
-                const float pv = ex2_mix<PolyPeriod<kD>::dq>(x / 2, fmaf(pr[x], sc, -lse2));
-                pr[x] = x > lim ? 0.0f : pv;
+            for (int x = 0; x < 64; ++x) pr[x] = ex2_mix<PolyPeriod<kD>::dq>(x / 2, fmaf(pr[x], sc, -lse2));
+            // masks only on the (warp-uniform) causal diagonal tile / the tile holding key N-1
+            if ((p.causal && j == i) || kbase + 64 > N) {
+#pragma unroll
+                for (int x = 0; x < 64; ++x)
+                    if (x > lim) pr[x] = 0.0f;
             }
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 1);
             mbar_wait<VATTN_SLEEP_MATH, true>(dp_full, j & 1);

@@ -77,9 +77,9 @@ __global__ void __launch_bounds__(384, 1)
 
     const int warp = warp_id();
     const int lane = lane_id();
-    const int bh = blockIdx.y;
-    const int nqb = gridDim.x;
-    const int qblk = p.causal ? (nqb - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
+    const int bh = grid_bh();
+    const int nqb = grid_ntiles();
+    const int qblk = p.causal ? (nqb - 1 - grid_tile()) : grid_tile();
     const int q0 = qblk * 256;
     const int N = p.N;
 
