@@ -649,10 +649,13 @@ __global__ void __launch_bounds__(384, 1)
                         dpv[x] = drop_keep(drow, col, p.drop_thresh) ? dpv[x] * p.inv_keep : 0.0f;
                     }
                 }
+                const float2 nd2 = make_float2(-dsum, -dsum);
 #pragma unroll
-                for (int x = 0; x < 16; ++x)
-                    dsp[16 * c + x] = pack2<kBF16>(pr[32 * c + 2 * x] * (dpv[2 * x] - dsum),
-                                                   pr[32 * c + 2 * x + 1] * (dpv[2 * x + 1] - dsum));
+                for (int x = 0; x < 16; ++x) {  // packed FADD2 / FMUL2: half the issue slots
+                    const float2 ds = fmul2(make_float2(pr[32 * c + 2 * x], pr[32 * c + 2 * x + 1]),
+                                            fadd2(make_float2(dpv[2 * x], dpv[2 * x + 1]), nd2));
+                    dsp[16 * c + x] = pack2<kBF16>(ds.x, ds.y);
+                }
             }
             tmem_st32(tmem + lb + R + 64 * h, dsp);  // dS over our (consumed) S columns
             tmem_wait_st();
