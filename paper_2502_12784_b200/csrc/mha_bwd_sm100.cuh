@@ -345,17 +345,19 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int x = 0; x < 32; x += 4) {
                     const float4 d4 = *reinterpret_cast<const float4*>(dsum + 32 * c + x);
-                    const float dvv[4] = {d4.x, d4.y, d4.z, d4.w};
-                    float ds[4];
+                    float dpd[4] = {dpv[x], dpv[x + 1], dpv[x + 2], dpv[x + 3]};
+                    if constexpr (kDrop) {  // dS = P o (drop o dP - D) (attention_backward.cpp:176-182)
 #pragma unroll
-                    for (int y = 0; y < 4; ++y) {
-                        float dpd = dpv[x + y];
-                        if constexpr (kDrop)  // dS = P o (drop o dP - D) (attention_backward.cpp:176-182)
-                            dpd = (keepm >> (32 * c + x + y)) & 1 ? dpd * p.inv_keep : 0.0f;
-                        ds[y] = pr[32 * c + x + y] * (dpd - dvv[y]);
+                        for (int y = 0; y < 4; ++y)
+                            dpd[y] = (keepm >> (32 * c + x + y)) & 1 ? dpd[y] * p.inv_keep : 0.0f;
                     }
-                    dsp[16 * c + x / 2] = pack2<kBF16>(ds[0], ds[1]);
-                    dsp[16 * c + x / 2 + 1] = pack2<kBF16>(ds[2], ds[3]);
+                    // packed FADD2 / FMUL2: half the issue slots
+                    const float2 s0 = fmul2(make_float2(pr[32 * c + x], pr[32 * c + x + 1]),
+                                            fadd2(make_float2(dpd[0], dpd[1]), make_float2(-d4.x, -d4.y)));
+                    const float2 s1 = fmul2(make_float2(pr[32 * c + x + 2], pr[32 * c + x + 3]),
+                                            fadd2(make_float2(dpd[2], dpd[3]), make_float2(-d4.z, -d4.w)));
+                    dsp[16 * c + x / 2] = pack2<kBF16>(s0.x, s0.y);
+                    dsp[16 * c + x / 2 + 1] = pack2<kBF16>(s1.x, s1.y);
                 }
             }
             tmem_st32(tmem + lb + Cfg::kTmemDP + 64 * h, dsp);  // dS^T over our dP^T columns
