@@ -96,11 +96,15 @@ struct BwdParams {
 // overlaps dK_i + dP_(i+1); the dS pass overlaps dV_(i+1) + S_(i+2).
 // Warps: 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 two warpgroups (thread = key row;
 // warpgroup h owns query columns [64h, 64h+64)).
+// d = 64 frees tensor memory for a second S^T region: S_(i+2) is computed while
+// the P pass of tile i+1 runs, so the P pass never waits for S (with a third Q/dO
+// stage so the load of Q_(i+2) does not wait for dK_i).  d = 128 keeps one region.
 template <int kD>
 struct DkdvCfg {
+    static constexpr bool kDoubleS = kD == 64;
     static constexpr int kTileBytes = kD * 128 * 2;
     static constexpr int kBoxes = kD / 64;
-    static constexpr int kStages = 2;
+    static constexpr int kStages = kDoubleS ? 3 : 2;
     static constexpr int kSmemK = 0;
     static constexpr int kSmemV = kTileBytes;
     static constexpr int kSmemQ = 2 * kTileBytes;
@@ -110,7 +114,9 @@ struct DkdvCfg {
     static constexpr int kSmemBar = kSmemDrop + 2048;
     static constexpr int kNumBars = 16;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
-    static constexpr uint32_t kTmemS = 0, kTmemDP = 128, kTmemDV = 256, kTmemDK = 256 + kD;
+    static constexpr uint32_t kTmemS = 0;                       // region r at 128 r
+    static constexpr uint32_t kTmemDP = kDoubleS ? 256 : 128;
+    static constexpr uint32_t kTmemDV = kTmemDP + 128, kTmemDK = kTmemDV + kD;
 };
 
 template <int kD, bool kBF16, bool kDrop>
@@ -136,8 +142,9 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* kv_full = bars;
     uint64_t* q_full = bars + 1;          // [kSt]
     uint64_t* q_empty = q_full + kSt;     // [kSt]
-    uint64_t* s_full = q_empty + kSt;
-    uint64_t* dp_full = s_full + 1;
+    constexpr bool kDB = Cfg::kDoubleS;
+    uint64_t* s_full = q_empty + kSt;     // [kDB ? 2 : 1] per S region
+    uint64_t* dp_full = s_full + (kDB ? 2 : 1);
     uint64_t* p_full = dp_full + 1;   // [warpgroup]
     uint64_t* ds_full = p_full + 2;   // [warpgroup]
     uint64_t* dkv_full = ds_full + 2;
@@ -160,6 +167,7 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(q_empty + s, 1 + 8);  // MMA commit + 8 warps done with lse2/D
         }
         mbar_init(s_full, 1);
+        if (kDB) mbar_init(s_full + 1, 1);
         mbar_init(dp_full, 1);
         for (int x = 0; x < 2; ++x) {
             mbar_init(p_full + x, 4);  // one arrive per warp of warpgroup x
@@ -240,6 +248,31 @@ __global__ void __launch_bounds__(384, 1)
         issue_kk(Cfg::kTmemDP, dV, dDOk);
         mma_commit_e(dp_full);
         VTRACE(3072);
+        if constexpr (kDB) {
+            if (n_steps > 1) {
+                mbar_wait_mma(q_full + 1, 0);
+                tc_fence_after();
+                issue_kk(Cfg::kTmemS + 128, dK, dQk + kTile16);  // S_1 into the second region
+                mma_commit_e(s_full + 1);
+            }
+            for (int s = 0; s < n_steps; ++s) {
+                const int st = s % kSt, st1 = (s + 1) % kSt, st2 = (s + 2) % kSt;
+                const uint32_t R = (s & 1) * 128u;
+                issue_ts(Cfg::kTmemDV, Cfg::kTmemS + R, dDOm + st * kTile16, s > 0, p_full, s & 1);  // dV += P^T dO
+                issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, s & 1);      // dK += dS^T Q
+                mma_commit_e(q_empty + st);
+                if (s + 1 < n_steps) {
+                    issue_kk(Cfg::kTmemDP, dV, dDOk + st1 * kTile16);  // after dK read dS^T
+                    mma_commit_e(dp_full);
+                }
+                if (s + 2 < n_steps) {  // region R is free once dV_s read P^T_s (in order)
+                    mbar_wait_mma(q_full + st2, ((s + 2) / kSt) & 1);
+                    tc_fence_after();
+                    issue_kk(Cfg::kTmemS + R, dK, dQk + st2 * kTile16);
+                    mma_commit_e(s_full + (s & 1));
+                }
+            }
+        } else
         for (int s = 0; s < n_steps; ++s) {
             const int st = s % kSt;
             const int st1 = (s + 1) % kSt;
@@ -277,13 +310,14 @@ __global__ void __launch_bounds__(384, 1)
             const int i = i0 + s;
             const float* lse2 = sLD + st * 256 + 64 * h;
             const float* dsum = sLD + st * 256 + 128 + 64 * h;
+            const uint32_t sR = Cfg::kTmemS + (kDB ? (s & 1) * 128u : 0u);  // S / P^T region of this tile
             mbar_wait(q_full + st, (s / kSt) & 1);  // lse2 / D of this tile landed
-            mbar_wait(s_full, s & 1);
+            mbar_wait(s_full + (kDB ? (s & 1) : 0), kDB ? ((s >> 1) & 1) : (s & 1));
             tc_fence_after();
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 0);
             float pr[64];
-            tmem_ld32f(tmem + lb + Cfg::kTmemS + 64 * h, pr);
-            tmem_ld32f(tmem + lb + Cfg::kTmemS + 64 * h + 32, pr + 32);
+            tmem_ld32f(tmem + lb + sR + 64 * h, pr);
+            tmem_ld32f(tmem + lb + sR + 64 * h + 32, pr + 32);
             tmem_wait_ld();
             const int qbase = i * 128 + 64 * h;
             uint64_t keepm = ~0ull;  // dropout keep bits of this thread's 64 (query, key) positions
@@ -325,7 +359,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                     for (int x = 0; x < 32; ++x) pk[x] = pack2<kBF16>(pr[2 * x], pr[2 * x + 1]);
                 }
-                tmem_st32(tmem + lb + Cfg::kTmemS + 64 * h, pk);  // own columns only
+                tmem_st32(tmem + lb + sR + 64 * h, pk);  // own columns only
             }
             tmem_wait_st();
             tc_fence_before();
