@@ -464,7 +464,10 @@ struct DqCfg {
     static constexpr int kSmemK = 2 * kTileBytes;
     static constexpr int kSmemV = kSmemK + kKSlots * kTileBytes;
     static constexpr int kSmemBar = kSmemV + kVSlots * kTileBytes;
-    static constexpr int kNumBars = 1 + 2 * kKSlots + 2 * kVSlots + 2 + 1 + 1 + 1;
+    static constexpr int kNumBars = 1 + 2 * kKSlots + 2 * kVSlots + 2 + 1 + 1 + 1 + 1;
+    // d = 64: dP_(j+1) is issued as soon as the math warps hold dP_j in registers
+    // (measured -4..5 % on the dQ kernel at d = 64; at d = 128 it delays S_(j+2) and loses)
+    static constexpr bool kEarlyDP = kD == 64;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr uint32_t kTmemDP = 256, kTmemDQ = 384;
 };
@@ -495,6 +498,7 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* dp_full = s_full + 2;
     uint64_t* ds_full = dp_full + 1;
     uint64_t* dq_done = ds_full + 1;
+    uint64_t* dp_empty = dq_done + 1;       // kEarlyDP: all 8 math warps loaded dP_j
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
     const int warp = warp_id();
@@ -521,6 +525,7 @@ __global__ void __launch_bounds__(384, 1)
         mbar_init(dp_full, 1);
         mbar_init(ds_full, 8);
         mbar_init(dq_done, 1);
+        mbar_init(dp_empty, 8);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -605,6 +610,16 @@ __global__ void __launch_bounds__(384, 1)
         for (int j = 0; j < nk; ++j) {
             const uint32_t R = (j & 1) ? 128u : 0u;
             const uint64_t kd = dKm + static_cast<uint64_t>(j % SK) * kTile16;
+            if constexpr (Cfg::kEarlyDP) {
+                if (j + 1 < nk) {  // the dP region is free once every math warp loaded dP_j
+                    mbar_wait_mma(dp_empty, j & 1);
+                    tc_fence_after();
+                    const uint64_t vo = vslot(j + 1);
+                    issue_kk(Cfg::kTmemDP, dDOd, dVk + vo);
+                    mma_commit_e(dp_full);
+                    mma_commit_e(v_empty + (j + 1) % SV);
+                }
+            }
             mbar_wait_mma(ds_full, j & 1);
             tc_fence_after();
             VTRACE(8 * j + 0);
@@ -618,7 +633,7 @@ __global__ void __launch_bounds__(384, 1)
             VTRACE(8 * j + 4);
             // dP_(j+1) after dQ_j (measured: issuing it first delays S_(j+2) and the
             // next P pass more than it shortens the dS chain)
-            if (j + 1 < nk) {
+            if (!Cfg::kEarlyDP && j + 1 < nk) {
                 const uint64_t vo = vslot(j + 1);
                 VTRACE(8 * j + 1);
                 issue_kk(Cfg::kTmemDP, dDOd, dVk + vo);
@@ -673,11 +688,25 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_after();
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 2);
             uint32_t dsp[32];
+            float dpa[Cfg::kEarlyDP ? 64 : 1];
+            if constexpr (Cfg::kEarlyDP) {
+                tmem_ld32f(tmem + lb + Cfg::kTmemDP + 64 * h, dpa);
+                tmem_ld32f(tmem + lb + Cfg::kTmemDP + 64 * h + 32, dpa + 32);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(dp_empty);  // the MMA warp may overwrite dP now
+            }
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                float dpv[32];
-                tmem_ld32f(tmem + lb + Cfg::kTmemDP + 64 * h + 32 * c, dpv);
-                tmem_wait_ld();
+                float dpb[32];
+                float* dpv = dpb;
+                if constexpr (Cfg::kEarlyDP) {
+                    dpv = dpa + 32 * c;
+                } else {
+                    tmem_ld32f(tmem + lb + Cfg::kTmemDP + 64 * h + 32 * c, dpb);
+                    tmem_wait_ld();
+                }
                 if constexpr (kDrop) {  // dS = P o (drop o dP - D)
 #pragma unroll
                     for (int x = 0; x < 32; ++x) {
