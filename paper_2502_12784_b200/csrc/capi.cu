@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 #include <string>
@@ -95,6 +96,19 @@ bool make_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16) 
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+// dS^T scratch viewed as [tiles][128 keys][128 queries] 16-bit, 64-query x 128-key boxes.
+bool make_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16) {
+    EncodeFn enc = encode_fn();
+    if (!enc || tiles > (1ll << 31) - 1) return false;
+    const cuuint64_t dims[3] = {128, 128, static_cast<cuuint64_t>(tiles)};
+    const cuuint64_t strides[2] = {256, 32768};
+    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(ptr),
+               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // sm_100 check, cached per device.
@@ -202,9 +216,17 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
 }
 
 struct BwdLayout {
-    size_t lse2, dsum, total;
+    size_t lse2, dsum, ds, total;
     int n_q, Npad;
+    bool materialize_ds;     // dQ as a GEMM over materialised dS (else recompute S, dP)
+    long long ds_tiles_per_bh;
 };
+
+// dS materialisation costs 32 KiB of workspace per (query tile, key tile) pair
+// (C3: 4.4 GB of a B200's 180 GB).  It is used at d = 128 while that stays under a
+// cap (C5 on one GPU would need 69 GB and recomputes; on 8 GPUs each shard needs
+// 8.6 GB).  VATTN_DQ_MODE=0/1 forces a mode (tuning and tests).
+constexpr size_t kDsCapBytes = 32ull << 30;
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -215,7 +237,21 @@ BwdLayout bwd_layout(const vattn_config* c) {
     L.Npad = L.n_q * 128;
     L.lse2 = 0;
     L.dsum = align256(BH * L.Npad * 4);
-    L.total = L.dsum + align256(BH * L.Npad * 4);
+    L.ds = L.dsum + align256(BH * L.Npad * 4);
+    const long long nq = L.n_q;
+    L.ds_tiles_per_bh = c->causal ? nq * (nq + 1) / 2 : nq * nq;
+    const size_t ds_bytes = BH * static_cast<size_t>(L.ds_tiles_per_bh) * 32768;
+    static const int mode_env = [] {
+        const char* e = getenv("VATTN_DQ_MODE");
+        return e ? atoi(e) : -1;
+    }();
+    // (the dK/dV kernel's dS^T staging overlaps its dropout row-hash buffer)
+    // d = 64 keeps the recompute path: its shorter dK/dV iterations pay more for the
+    // staging than the dQ GEMM saves (measured: C2 -3 %, C3 at d = 128 +8 %).
+    L.materialize_ds = c->dropout_p > 0.0f
+                           ? false
+                           : (mode_env >= 0 ? mode_env == 1 : (c->head_dim == 128 && ds_bytes <= kDsCapBytes));
+    L.total = L.ds + (L.materialize_ds ? align256(ds_bytes) : 0);
     return L;
 }
 
@@ -263,6 +299,11 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     p.scale = eff_scale(c);
     p.scale_log2 = p.scale * kLog2e;
     set_dropout(c, &p.H, &p.bh_off, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
+    p.ds_out = L.materialize_ds ? reinterpret_cast<uint16_t*>(w + L.ds) : nullptr;
+    p.ds_tiles_per_bh = L.ds_tiles_per_bh;
+    CUtensorMap mds;
+    if (L.materialize_ds && !make_ds_map(&mds, p.ds_out, static_cast<long long>(BH) * L.ds_tiles_per_bh, kBF16))
+        return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled (dS) failed");
     // 2) dK, dV (key-major)
     {
         auto kern = mha_bwd_dkdv_kernel<kD, kBF16, kDrop>;
@@ -270,10 +311,17 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
-        kern<<<tile_grid(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, dk, dv, p);
+        kern<<<tile_grid(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, L.materialize_ds ? mds : mq, dk, dv, p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)
-    {
+    if (L.materialize_ds) {
+        auto kern = mha_bwd_dq_gemm_kernel<kD, kBF16>;
+        constexpr int smem = DqGemmCfg<kD>::kSmemBytes;
+        const cudaError_t ae = set_smem_once<mha_bwd_dq_gemm_kernel<kD, kBF16>>(smem);
+        if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
+        ProfScope prof(stream, 2);
+        kern<<<tile_grid(L.n_q, BH), 256, smem, stream>>>(mds, mk, mdq, p);
+    } else {
         auto kern = mha_bwd_dq_kernel<kD, kBF16, kDrop>;
         constexpr int smem = DqCfg<kD>::kSmemBytes;
         const cudaError_t ae = set_smem_once<mha_bwd_dq_kernel<kD, kBF16, kDrop>>(smem);

@@ -81,7 +81,17 @@ struct BwdParams {
     float inv_keep;     // 1 / (1 - dropout_p)
     uint64_t drop_seed;
     uint64_t drop_thresh;
+    // dS materialisation (optional): the dK/dV kernel also writes every dS^T tile
+    // (16-bit, [128 keys][128 queries]) here and dQ = dS K becomes a streaming GEMM
+    // (mha_bwd_dq_gemm_kernel) instead of the recomputing dQ kernel.  nullptr = off.
+    uint16_t* ds_out;
+    long long ds_tiles_per_bh;  // n_q^2, or n_q (n_q + 1) / 2 causal (lower triangle)
 };
+
+// Index of dS^T tile (query tile i, key tile kb) within one (b, h).
+VATTN_DEV long long ds_tile_index(const BwdParams& p, int i, int kb) {
+    return p.causal ? static_cast<long long>(i) * (i + 1) / 2 + kb : static_cast<long long>(i) * p.n_q + kb;
+}
 
 // ================================================================ dK / dV ==
 //
@@ -111,7 +121,10 @@ struct DkdvCfg {
     static constexpr int kSmemDO = kSmemQ + kStages * kTileBytes;
     static constexpr int kSmemLD = kSmemDO + kStages * kTileBytes;  // [stage][lse2 128 | D 128]
     static constexpr int kSmemDrop = kSmemLD + kStages * 1024;      // dropout row hashes [128] x 16 B
-    static constexpr int kSmemBar = kSmemDrop + 2048;
+    // dS^T staging for its TMA store (dS materialisation, 2 boxes of 64 queries x 128
+    // keys).  It overlaps the dropout row hashes: materialisation is off with dropout.
+    static constexpr int kSmemDsStage = kSmemDrop;
+    static constexpr int kSmemBar = kSmemDsStage + 32768;
     static constexpr int kNumBars = 16;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr uint32_t kTmemS = 0;                       // region r at 128 r
@@ -124,7 +137,8 @@ __global__ void __launch_bounds__(384, 1)
     mha_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v,
-                        const __grid_constant__ CUtensorMap tm_do, void* __restrict__ dk_out,
+                        const __grid_constant__ CUtensorMap tm_do,
+                        const __grid_constant__ CUtensorMap tm_ds, void* __restrict__ dk_out,
                         void* __restrict__ dv_out, const BwdParams p) {
     using Cfg = DkdvCfg<kD>;
     constexpr int kVtraceKid = 1;
@@ -394,6 +408,25 @@ __global__ void __launch_bounds__(384, 1)
                     dsp[16 * c + x / 2 + 1] = pack2<kBF16>(s1.x, s1.y);
                 }
             }
+            const bool ds_store_thread = (warp & 3) == 0 && lane == 0;  // one per warpgroup
+            if (p.ds_out) {
+                // dS^T tile -> swizzled smem box (this warpgroup's 64 queries x 128 keys) ->
+                // TMA store, off the critical path (replaces 16-byte global stores that
+                // stalled the dS pass)
+                uint8_t* box = smem + Cfg::kSmemDsStage + h * 16384;
+                if (ds_store_thread) bulk_wait_read0();  // the previous box left the buffer
+                named_bar_sync(1 + h, 128);
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+                    st_swz128(box, r, m, make_uint4(dsp[4 * m], dsp[4 * m + 1], dsp[4 * m + 2], dsp[4 * m + 3]));
+                fence_proxy_async_smem();
+                named_bar_sync(1 + h, 128);
+                if (ds_store_thread) {
+                    tma_store_3d(&tm_ds, box, 64 * h, 0,
+                                 static_cast<int>(static_cast<long long>(bh) * p.ds_tiles_per_bh + ds_tile_index(p, i, kb)));
+                    bulk_commit();
+                }
+            }
             tmem_st32(tmem + lb + Cfg::kTmemDP + 64 * h, dsp);  // dS^T over our dP^T columns
             tmem_wait_st();
             tc_fence_before();
@@ -404,6 +437,7 @@ __global__ void __launch_bounds__(384, 1)
             }
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 3);
         }
+        if (p.ds_out && (warp & 3) == 0 && lane == 0) bulk_wait_read0();  // no store reads smem past exit
         // ---------------------------------------------------------- epilogue
         mbar_wait(dkv_full, 0);
         tc_fence_after();
@@ -763,6 +797,130 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
+    }
+}
+
+// ============================================================ dQ = dS K ==
+//
+// With dS materialised by the dK/dV kernel, dQ_i = sum_j dS_ij K_j is a plain
+// streaming GEMM: one CTA per (b*h, 128-query tile i), dS_ij (from its dS^T tile,
+// an MN-major A operand) and K_j (MN-major B) through a TMA ring, accumulated in
+// tensor memory in ascending j (the same fixed order and single rounding as the
+// reference's DqAccumulator, attention_backward.cpp:205,215) -- deterministic, and
+// none of the S / dP recompute of mha_bwd_dq_kernel.  HBM-bound on the dS stream.
+template <int kD>
+struct DqGemmCfg {
+    static constexpr int kKBytes = kD * 128 * 2;
+    static constexpr int kDsBytes = 128 * 128 * 2;
+    static constexpr int kStageBytes = kKBytes + kDsBytes;
+    static constexpr int kStages = kD == 128 ? 3 : 4;
+    static constexpr int kSmemBar = kStages * kStageBytes;
+    static constexpr int kNumBars = 2 * kStages + 1;
+    static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
+};
+
+template <int kD, bool kBF16>
+__global__ void __launch_bounds__(256, 1)
+    mha_bwd_dq_gemm_kernel(const __grid_constant__ CUtensorMap tm_ds, const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
+    using Cfg = DqGemmCfg<kD>;
+    constexpr int S = Cfg::kStages;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kSmemBar);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* dq_done = bars + 2 * S;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
+    const int warp = warp_id();
+    const int lane = lane_id();
+    const int bh = grid_bh();
+    const int nqb = grid_ntiles();
+    const int i = p.causal ? (nqb - 1 - grid_tile()) : grid_tile();
+    const int nk = p.causal ? i + 1 : p.n_q;
+    if (threadIdx.x == 0) {
+        if ((smem_u32(smem) & 1023u) != 0) __trap();
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(dq_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<kD>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tm_ds);
+            tma_prefetch_desc(&tm_k);
+            tma_prefetch_desc(&tm_dq);
+            const long long tile0 = static_cast<long long>(bh) * p.ds_tiles_per_bh + ds_tile_index(p, i, 0);
+            for (int j = 0; j < nk; ++j) {
+                const int st = j % S;
+                mbar_wait<VATTN_SLEEP_PRODUCER>(empty + st, ((j / S) & 1) ^ 1);
+                mbar_arrive_expect_tx(full + st, Cfg::kStageBytes);
+                uint8_t* ds = smem + st * Cfg::kStageBytes;
+                uint8_t* kt = ds + Cfg::kDsBytes;
+                const int tile = static_cast<int>(tile0 + j);
+                tma_load_3d(ds, &tm_ds, full + st, 0, 0, tile);
+                tma_load_3d(ds + 16384, &tm_ds, full + st, 64, 0, tile);
+                for (int b = 0; b < kD / 64; ++b) tma_load_3d(kt + b * 16384, &tm_k, full + st, b * 64, j * 128, bh);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = umma_idesc_f16(128, kD, kBF16, 1, 1);  // A = dS (MN-major), B = K (MN-major)
+        const uint64_t dA0 = umma_desc_sw128(smem_u32(smem), 16384, 1024);
+        const uint64_t dB0 = umma_desc_sw128(smem_u32(smem + Cfg::kDsBytes), 16384, 1024);
+        constexpr uint64_t kStage16 = Cfg::kStageBytes >> 4;
+        for (int j = 0; j < nk; ++j) {
+            const int st = j % S;
+            mbar_wait_mma(full + st, (j / S) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                mma_ss_e(tmem, desc_mnmajor(dA0 + st * kStage16, kk), desc_mnmajor(dB0 + st * kStage16, kk), idesc,
+                         (j > 0 || kk > 0) ? 1u : 0u);
+            mma_commit_e(empty + st);
+        }
+        mma_commit_e(dq_done);
+    } else if (warp >= 4) {
+        // epilogue: dQ * scale -> 16-bit -> swizzled smem (stage 0's dS buffer) -> TMA store
+        const int r = ((warp & 3) << 5) + lane;
+        const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        mbar_wait<VATTN_SLEEP_MATH>(dq_done, 0);
+        tc_fence_after();
+        uint8_t* sOut = smem;
+#pragma unroll
+        for (int c = 0; c < kD / 32; ++c) {
+            float a[32];
+            tmem_ld32f(tmem + lb + 32 * c, a);
+            tmem_wait_ld();
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                uint4 v;
+                v.x = pack2<kBF16>(a[8 * x + 0] * p.scale, a[8 * x + 1] * p.scale);
+                v.y = pack2<kBF16>(a[8 * x + 2] * p.scale, a[8 * x + 3] * p.scale);
+                v.z = pack2<kBF16>(a[8 * x + 4] * p.scale, a[8 * x + 5] * p.scale);
+                v.w = pack2<kBF16>(a[8 * x + 6] * p.scale, a[8 * x + 7] * p.scale);
+                const int cc = 32 * c + 8 * x;
+                st_swz128(sOut + (cc >> 6) * 16384, r, (cc & 63) >> 3, v);
+            }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (warp == 4 && lane == 0) {
+            for (int b = 0; b < kD / 64; ++b) tma_store_3d(&tm_dq, sOut + b * 16384, b * 64, i * 128, bh);
+            bulk_commit();
+            bulk_wait_read0();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<kD>(tmem);
     }
 }
 

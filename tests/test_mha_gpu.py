@@ -282,3 +282,38 @@ def test_dropout_random_vs_binary64_and_deterministic(B, H, N, d, causal, dtype)
     o2, _ = vb.mha_forward(q, k, v, causal, dropout_p=p, seed=seed)
     g2 = vb.mha_backward(q, k, v, o, do, lse, causal, dropout_p=p, seed=seed)
     assert torch.equal(o, o2) and all(torch.equal(a, b) for a, b in zip((dq, dk, dv), g2))
+
+
+# ------------------------------------------------------ dQ computation modes --
+_DQ_MODE_CHILD = r'''
+import os, sys
+sys.path.insert(0, os.environ["ROOT"])
+import torch
+import paper_2502_12784_b200 as vb
+from oracle import pyoracle as po
+from tests.gpu_util import check_close, widen, workload
+for (B, H, N, d, causal, dtype) in [(1, 2, 384, 128, True, torch.bfloat16), (2, 1, 260, 128, False, torch.float16),
+                                    (1, 2, 384, 64, True, torch.float16)]:
+    q, k, v, do = workload(13 + N, (B, H, N, d), dtype)
+    o, lse = vb.mha_forward(q, k, v, causal)
+    dq, dk, dv = vb.mha_backward(q, k, v, o, do, lse, causal)
+    rdq, rdk, rdv = po.attention_grad_ref(widen(q), widen(k), widen(v), widen(do), causal)
+    for name, t, r in (("dQ", dq, rdq), ("dK", dk, rdk), ("dV", dv, rdv)):
+        check_close(widen(t), r, dtype, name + " mode " + os.environ["VATTN_DQ_MODE"])
+    a = vb.mha_backward(q, k, v, o, do, lse, causal)
+    assert all(torch.equal(x, y) for x, y in zip((dq, dk, dv), a)), "not deterministic"
+print("OK")
+'''
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_dq_modes_vs_binary64(mode):
+    """dQ by recompute (mode 0, mha_bwd_dq_kernel) and from materialised dS (mode 1,
+    mha_bwd_dq_gemm_kernel) both meet the binary64 tolerances and are deterministic.
+    The mode is read once per process, hence the subprocess."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _DQ_MODE_CHILD], env=dict(os.environ, VATTN_DQ_MODE=mode, ROOT=root),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
