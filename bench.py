@@ -232,7 +232,7 @@ def main():
 
     # ---------------------------------------------------------------- timed
     vb.lib.vattn_profile_enable(1)
-    launches_per_step = 4  # fwd + (preprocess, dK/dV kernel, dQ kernel)
+    launches_per_step = 4  # fwd + (preprocess, dK/dV kernel, dQ kernel or dQ GEMM)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -298,6 +298,13 @@ def main():
         # dominant kernel: the key-major dK/dV kernel (4 of the 5 algorithmic
         # backward GEMMs: S^T, dP^T, dV, dK = 8 B H N^2 d c flops per launch)
         f_dkdv = 0.8 * f_bwd
+        # dQ path the library chose: the workspace holds materialised dS^T tiles
+        # (d = 128 under the cap) beyond lse2 + D (8 B per padded row)
+        n_q = (N + 127) // 128
+        base_ws = 2 * ((B * H * n_q * 128 * 4 + 255) // 256 * 256)
+        tiles = B * H * (n_q * (n_q + 1) // 2 if causal else n_q * n_q)
+        ds_bytes = tiles * 32768
+        dq_mode = "dS-GEMM" if ws.numel() > base_ws + 256 else "recompute"
         achieved = f_dkdv / (dkdv_ms * 1e-3) / 1e12
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -321,7 +328,13 @@ def main():
                            "bwd_other(preprocess)": ms_step - fwd_ms - dkdv_ms - dq_ms},
             "fwd_tflops": f_fwd / (fwd_ms * 1e-3) / 1e12,
             "bwd_tflops": f_bwd / ((ms_step - fwd_ms) * 1e-3) / 1e12,
-            "dq_kernel_tflops_executed": 0.6 * f_bwd / (dq_ms * 1e-3) / 1e12,
+            "bwd_dq_mode": dq_mode,
+            "dq_kernel": ({"kernel": "mha_bwd_dq_gemm_kernel", "bound": "hbm",
+                           "achieved_gbs": ds_bytes / (dq_ms * 1e-3) / 1e9,
+                           "bytes_note": "dS^T tiles streamed once (16-bit, 32 KiB per tile pair)"}
+                          if dq_mode == "dS-GEMM" else
+                          {"kernel": "mha_bwd_dq_kernel", "bound": "tensor",
+                           "tflops_executed": 0.6 * f_bwd / (dq_ms * 1e-3) / 1e12}),
             "roofline": {"kernel": "mha_bwd_dkdv_kernel", "bound": "tensor", "achieved": achieved,
                          "peak": peak_sust, "peak_kind": f"bf16_tflops_sustained ({peak_src})",
                          "unit": "TFLOP/s", "frac": achieved / peak_sust, "frac_of_burst": achieved / peak_burst,

@@ -45,6 +45,7 @@ SHORT = {
     "mha_fwd_sm100_kernel": "fwd",
     "mha_bwd_dkdv_kernel": "bwd_dkdv",
     "mha_bwd_dq_kernel": "bwd_dq",
+    "mha_bwd_dq_gemm_kernel": "bwd_dq_gemm",
     "mha_bwd_preprocess_kernel": "bwd_preprocess",
 }
 
