@@ -408,6 +408,15 @@ __global__ void __launch_bounds__(384, 1)
                     dsp[16 * c + x / 2 + 1] = pack2<kBF16>(s1.x, s1.y);
                 }
             }
+            tmem_st32(tmem + lb + Cfg::kTmemDP + 64 * h, dsp);  // dS^T over our dP^T columns
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(ds_full + h);
+                mbar_arrive(q_empty + st);  // done with lse2 / D of this stage
+            }
+            // dS^T materialisation after publishing: dK_i starts while the tile is staged
             const bool ds_store_thread = (warp & 3) == 0 && lane == 0;  // one per warpgroup
             if (p.ds_out) {
                 // dS^T tile -> swizzled smem box (this warpgroup's 64 queries x 128 keys) ->
@@ -427,14 +436,7 @@ __global__ void __launch_bounds__(384, 1)
                     bulk_commit();
                 }
             }
-            tmem_st32(tmem + lb + Cfg::kTmemDP + 64 * h, dsp);  // dS^T over our dP^T columns
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(ds_full + h);
-                mbar_arrive(q_empty + st);  // done with lse2 / D of this stage
-            }
+
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 3);
         }
         if (p.ds_out && (warp & 3) == 0 && lane == 0) bulk_wait_read0();  // no store reads smem past exit
