@@ -344,7 +344,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only (a reported baseline)
             try:
                 tfl, secs, sample, kind, cores = cpu_reference_sample(d, causal, os.cpu_count() or 1)
                 line["cpu_baseline"] = {"value": tfl, "unit": "TFLOPS", "cores": cores, "kind": kind, "sample": sample}
