@@ -231,7 +231,8 @@ def main():
     torch.cuda.synchronize()
 
     # ---------------------------------------------------------------- timed
-    vb.lib.vattn_profile_enable(1)
+    # (no per-kernel events inside the timed region: an event between two kernels
+    # would break their programmatic-dependent-launch overlap)
     launches_per_step = 4  # fwd + (preprocess, dK/dV kernel, dQ kernel or dQ GEMM)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -246,7 +247,13 @@ def main():
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(stop)
+    # per-kernel durations (roofline): a separate profiled pass, CUDA events on the
+    # launching stream around each hot kernel
     import ctypes as C
+    vb.lib.vattn_profile_enable(1)
+    for _ in range(max(3, min(args.steps, 10))):
+        step()
+    torch.cuda.synchronize()
     kern_ms = []
     for kind in (0, 1, 2):  # VATTN_KERNEL_FWD, _BWD_DKDV, _BWD_DQ
         t_ms, n_l = C.c_double(), C.c_int()

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/vattn_b200.h"
@@ -22,6 +23,7 @@ using namespace vattn_sm100;
 namespace {
 
 thread_local std::string g_err;
+thread_local cudaError_t g_launch_err = cudaSuccess;
 thread_local int g_launches = 0;
 
 // ---- measurement hooks (vattn_profile_*): event pairs around the hot kernels
@@ -181,6 +183,27 @@ void set_dropout(const vattn_config* c, int* H, int* bh_off, float* inv_keep, ui
     *thresh = static_cast<uint64_t>(std::ceil(static_cast<double>(c->dropout_p) * 9007199254740992.0));
 }
 
+// Launch with programmatic stream serialisation (see griddep_* in sm100_ptx.cuh):
+// the kernel's CTAs may start their prologue while the previous kernel drains.
+template <typename... Params, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, int smem, cudaStream_t stream,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+    if (e != cudaSuccess) g_launch_err = e;  // reported by the call's final error check
+    return e;
+}
+
+
 template <int kD, bool kBF16, bool kDrop>
 int launch_forward(const vattn_config* c, const void* q, const void* k, const void* v, void* o,
                    float* lse, cudaStream_t stream) {
@@ -207,9 +230,11 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     const dim3 grid = tile_grid((N + 255) / 256, BH);
     {
         ProfScope prof(stream, 0);
-        kern<<<grid, FwdCfg<kD>::kThreads, smem, stream>>>(mq, mk, mv, mo, p);
+        launch_pdl(kern, grid, dim3(FwdCfg<kD>::kThreads), smem, stream, mq, mk, mv, mo, p);
     }
-    const cudaError_t e = cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = g_launch_err;
+    g_launch_err = cudaSuccess;
     if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("mha_fwd launch: ") + cudaGetErrorString(e));
     g_launches = 1;
     return VATTN_OK;
@@ -286,8 +311,8 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const long long rows = static_cast<long long>(BH) * L.Npad;
         long long blocks = (rows + 7) / 8;
         if (blocks > 148 * 16) blocks = 148 * 16;
-        mha_bwd_preprocess_kernel<kD, kBF16><<<static_cast<int>(blocks), 256, 0, stream>>>(
-            o, dout, lse, lse2, dsum, N, L.Npad, BH);
+        launch_pdl(mha_bwd_preprocess_kernel<kD, kBF16>, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream,
+                   o, dout, lse, lse2, dsum, N, L.Npad, BH);
     }
     BwdParams p;
     p.lse2 = lse2;
@@ -311,7 +336,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
-        kern<<<tile_grid(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, L.materialize_ds ? mds : mq, dk, dv, p);
+        launch_pdl(kern, tile_grid(L.n_q, BH), dim3(384), smem, stream, mq, mk, mv, mdo, L.materialize_ds ? mds : mq, dk, dv, p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)
     if (L.materialize_ds) {
@@ -320,16 +345,18 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const cudaError_t ae = set_smem_once<mha_bwd_dq_gemm_kernel<kD, kBF16>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 2);
-        kern<<<tile_grid(L.n_q, BH), 256, smem, stream>>>(mds, mk, mdq, p);
+        launch_pdl(kern, tile_grid(L.n_q, BH), dim3(256), smem, stream, mds, mk, mdq, p);
     } else {
         auto kern = mha_bwd_dq_kernel<kD, kBF16, kDrop>;
         constexpr int smem = DqCfg<kD>::kSmemBytes;
         const cudaError_t ae = set_smem_once<mha_bwd_dq_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 2);
-        kern<<<tile_grid(L.n_q, BH), 384, smem, stream>>>(mq, mk, mv, mdo, mdq, p);
+        launch_pdl(kern, tile_grid(L.n_q, BH), dim3(384), smem, stream, mq, mk, mv, mdo, mdq, p);
     }
-    const cudaError_t e = cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = g_launch_err;
+    g_launch_err = cudaSuccess;
     if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("mha_bwd launch: ") + cudaGetErrorString(e));
     g_launches = 3;
     return VATTN_OK;

@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(256) mha_bwd_preprocess_kernel(
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const long long rows = static_cast<long long>(BH) * Npad;
+    griddep_wait();  // O / lse come from the forward kernel
     for (long long r0 = static_cast<long long>(gw) * kRowsPerWarp; r0 < rows;
          r0 += static_cast<long long>(nwarps) * kRowsPerWarp) {
         const long long row = r0 + lane / kLanesPerRow;
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(256) mha_bwd_preprocess_kernel(
             lse2[row] = valid ? lse[static_cast<size_t>(bh) * N + n] * 1.4426950408889634f : INFINITY;
         }
     }
+    griddep_launch_dependents();
 }
 
 struct BwdParams {
@@ -195,6 +197,7 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait();  // inputs written by the previous kernel in the stream are visible
     if (warp < 4) regs_dec<88>();
 
     if (warp == 0) {
@@ -470,6 +473,7 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     }
+    griddep_launch_dependents();
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -569,6 +573,7 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait();  // inputs written by the previous kernel in the stream are visible
     if (warp < 4) regs_dec<88>();
 
     if (warp == 0) {
@@ -794,6 +799,7 @@ __global__ void __launch_bounds__(384, 1)
             bulk_wait_read0();
         }
     }
+    griddep_launch_dependents();
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -853,6 +859,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait();  // inputs written by the previous kernel in the stream are visible
     if (warp == 0) {
         if (lane == 0) {
             tma_prefetch_desc(&tm_ds);
@@ -918,6 +925,7 @@ __global__ void __launch_bounds__(256, 1)
             bulk_wait_read0();
         }
     }
+    griddep_launch_dependents();
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait();  // inputs written by the previous kernel in the stream are visible
     // registers: producer/MMA warpgroup 88, softmax warpgroups 208 (384 x 168 budget);
     // each role lowers/raises its own budget inside its branch.
     if (warp < 4) regs_dec<88>();
@@ -384,6 +385,7 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     }
+    griddep_launch_dependents();
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {

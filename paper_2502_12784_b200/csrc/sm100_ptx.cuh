@@ -42,6 +42,16 @@ VATTN_DEV void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :
 template <uint32_t kRegs>
 VATTN_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs)); }
 
+// Programmatic dependent launch: kernels are launched with programmatic stream
+// serialisation, so the next kernel's CTAs set up (barriers, tensor memory) while
+// this grid's last CTAs finish.  griddep_wait() blocks until the previous grid in
+// the stream completed and its writes are visible -- every kernel calls it before
+// its first global read; griddep_launch_dependents() at the end of every CTA lets
+// the next grid launch once all CTAs of this one reached it (never earlier, so a
+// waiting dependent can not take the SMs the remaining CTAs of this grid need).
+VATTN_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+VATTN_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Named barrier over `nthreads` threads (id 0 is __syncthreads).
 VATTN_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

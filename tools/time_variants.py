@@ -35,12 +35,14 @@ for name in os.environ["CFGS"].split(","):
     for _ in range(3): step()
     torch.cuda.synchronize()
     steps = int(os.environ["STEPS"])
-    vb.lib.vattn_profile_enable(1)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(steps): step()
     b.record(); torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
+    vb.lib.vattn_profile_enable(1)
+    for _ in range(5): step()
+    torch.cuda.synchronize()
     ks = []
     for kind in (0, 1, 2):
         t, n = C.c_double(), C.c_int()
