@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -106,9 +107,14 @@ int units_of(const vattn_config* c) { return c->bh_count ? c->bh_count : c->batc
 // Slab size: every launch should still fill the GPU (>= 2 CTAs per SM over the
 // 128-row tiles of a head) while keeping enough slabs for the copies to overlap.
 int slab_units(const vattn_config* c, int U) {
+    static const int env = [] {  // tuning override: slabs per call
+        const char* e = getenv("VATTN_HOST_SLABS");
+        return e ? atoi(e) : 0;
+    }();
     const int tiles = (c->seq_len + 127) / 128;
     const int fill = (2 * 148 + tiles - 1) / tiles;
     const int for_overlap = (U + 15) / 16;  // aim for >= 16 slabs
+    if (env > 0) return std::max(1, (U + env - 1) / env);
     return std::max(1, std::min(U, std::max(fill, for_overlap)));
 }
 
