@@ -98,6 +98,20 @@ int mha_backward(const vattn_config* cfg, const void* q, const void* k, const vo
                  const void* o, const void* dout, const float* lse, void* dq, void* dk, void* dv,
                  void* workspace, size_t workspace_bytes, void* stream);
 
+/* D = rowsum(dO o O) per query row ([B, H, N] binary32, products widened before the
+ * sum) -- vattn::compute_dpsum (proj/include/vattn/backward.hpp:43,
+ * attention_backward.cpp:44-57), the backward's preprocessing pass on its own. */
+int mha_dpsum(const vattn_config* cfg, const void* o, const void* dout, float* d_rows, void* stream);
+
+/* The reference's dropout mask digest (ForwardOutput/GradOutputs::mask_digest,
+ * attention.hpp:32): the order-independent 64-bit sum of dropout_digest_term over
+ * the mask positions a pass with (tile_rows x tile_cols) tiles consumes -- the fused
+ * passes' visited tile pairs (tile_rows = tile_cols = N, causal = 0 gives the
+ * traditional pass's N x N).  Written to the device word `digest`; 0 when
+ * dropout_p == 0.  Bit-identical to the reference's value. */
+int vattn_dropout_digest(const vattn_config* cfg, int tile_rows, int tile_cols, unsigned long long* digest,
+                         void* stream);
+
 /* ---- host-buffer entry points (the reference's synchronous host API) ------
  * Same math as the device entry points, but every tensor is a HOST pointer
  * (pinned memory gives full copy/compute overlap; pageable memory works but

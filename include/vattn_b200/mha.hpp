@@ -93,7 +93,7 @@ struct ForwardOutput {
     std::vector<uint16_t> out;  // [B, H, N, d] 16-bit bit patterns
     std::vector<float> lse;     // [B, H, N]
     TrafficCounter traffic;     // closed forms of attention.hpp:40-50
-    uint64_t mask_digest = 0;   // tiling-dependent reference test hook: not produced
+    uint64_t mask_digest = 0;   // the reference's dropout digest over the visited tiles (vattn_dropout_digest)
 };
 
 struct GradOutputs {
@@ -194,6 +194,20 @@ inline vattn_config to_c(const AttnConfig& c, int dn) {
     return r;
 }
 
+// The reference's mask_digest for a pass with (tile_rows x tile_cols) tiles (0 when
+// dropout_p == 0): C ABI vattn_dropout_digest, bit-identical to the reference.
+inline uint64_t mask_digest(const vattn_config& c, int tile_rows, int tile_cols) {
+    if (c.dropout_p <= 0.0f) return 0;
+    unsigned long long* d = nullptr;
+    cuda(cudaMalloc(reinterpret_cast<void**>(&d), sizeof(unsigned long long)), "cudaMalloc");
+    const int rc = vattn_dropout_digest(&c, tile_rows, tile_cols, d, nullptr);
+    unsigned long long h = 0;
+    if (rc == VATTN_OK) cuda(cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost), "D2H digest");
+    cudaFree(d);
+    check(rc, "vattn_dropout_digest");
+    return h;
+}
+
 }  // namespace detail
 
 // ---------------------------------------------------------- device overloads
@@ -236,6 +250,7 @@ inline ForwardOutput forward_fused(const std::vector<uint16_t>& q, const std::ve
     r.lse.resize(rows);
     r.traffic = traffic_forward_fused(cfg);
     const vattn_config c = detail::to_c(cfg, dn);
+    r.mask_digest = detail::mask_digest(c, cfg.tile_rows, cfg.tile_cols);
     if (dn == cfg.head_dim) {
         detail::check(mha_forward_host(&c, q.data(), k.data(), v.data(), r.out.data(), r.lse.data(), nullptr),
                       "mha_forward_host");
@@ -284,6 +299,7 @@ inline GradOutputs backward_fused(const std::vector<uint16_t>& q, const std::vec
                   "mha_backward");
     GradOutputs g;
     g.traffic = traffic_backward_fused(cfg);
+    g.mask_digest = detail::mask_digest(c, cfg.tile_rows, cfg.tile_cols);
     g.dq.resize(cfg.elems());
     g.dk.resize(cfg.elems());
     g.dv.resize(cfg.elems());

@@ -27,7 +27,7 @@ extern "C" {
 /* Device workspace for S (binary32, B*H*N*N) and P (16-bit, B*H*N*N); 0 on bad cfg. */
 size_t mha_forward_traditional_workspace_bytes(const vattn_config* cfg);
 
-/* O, lse of the three-pass forward.  Device pointers, stream ordered.  (The
+/* O, lse of the three-pass forward (any head_dim with head_dim % 4 == 0, as the reference).  Device pointers, stream ordered.  (The
  * reference's fully-masked-row domain_error, attention_forward.cpp:279-280, cannot
  * occur: a top-left causal row always sees key 0.) */
 int mha_forward_traditional(const vattn_config* cfg, const void* q, const void* k, const void* v,

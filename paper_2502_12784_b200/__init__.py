@@ -32,7 +32,7 @@ import torch
 __all__ = [
     "AttnConfig", "forward_fused", "backward_fused", "mha_forward", "mha_backward",
     "workspace_bytes", "MHAFunction", "attention", "LIB_PATH", "lib",
-    "mha_forward_host", "mha_backward_host", "mha_step_host",
+    "mha_forward_host", "mha_backward_host", "mha_step_host", "compute_dpsum",
 ]
 
 LIB_PATH = os.environ.get("VATTN_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvattn_b200.so")
@@ -68,6 +68,8 @@ def _load():
     lib.mha_backward_host.restype = C.c_int
     lib.mha_step_host.argtypes = [C.POINTER(_Cfg)] + [vp] * 10
     lib.mha_step_host.restype = C.c_int
+    lib.mha_dpsum.argtypes = [C.POINTER(_Cfg)] + [vp] * 4
+    lib.mha_dpsum.restype = C.c_int
     lib.vattn_last_error.restype = C.c_char_p
     lib.vattn_abi_version.restype = C.c_int
     lib.vattn_last_launch_count.restype = C.c_int
@@ -289,6 +291,19 @@ def mha_step_host(q, k, v, dout, causal: bool = False, softmax_scale: float = 0.
     if rc:
         _raise(rc, "mha_step_host")
     return o, lse, dq, dk, dv
+
+
+def compute_dpsum(d_out, out):
+    """vattn::compute_dpsum (backward.hpp:43): D = rowsum(dO o O) as [B, H, N] fp32
+    (C ABI ``mha_dpsum``; head_dim 64 or 128)."""
+    _check((d_out, out), out.shape, out.dtype, ("d_out", "out"))
+    B, H, N, d = out.shape
+    D = torch.empty((B, H, N), dtype=torch.float32, device=out.device)
+    cfg = _cfg(out, False, 0.0)
+    rc = lib.mha_dpsum(C.byref(cfg), out.data_ptr(), d_out.data_ptr(), D.data_ptr(), _stream())
+    if rc:
+        _raise(rc, "mha_dpsum")
+    return D
 
 
 # ----------------------------------------- reference-shaped operator API --

@@ -17,6 +17,7 @@
 #include "../../include/vattn_b200.h"
 #include "mha_bwd_sm100.cuh"
 #include "mha_fwd_sm100.cuh"
+#include "dropout_digest.cuh"
 
 using namespace vattn_sm100;
 
@@ -442,6 +443,68 @@ int mha_forward(const vattn_config* cfg, const void* q, const void* k, const voi
         case 6: return launch_forward<128, true, false>(cfg, q, k, v, o, lse, s);
         default: return launch_forward<128, true, true>(cfg, q, k, v, o, lse, s);
     }
+}
+
+int mha_dpsum(const vattn_config* cfg, const void* o, const void* dout, float* d_rows, void* stream) {
+    g_launches = 0;
+    int rc = validate(cfg);
+    if (rc) return rc;
+    if (!o || !dout || !d_rows) return fail(VATTN_EINVAL, "mha_dpsum: null pointer");
+    if (!aligned16(o) || !aligned16(dout)) return fail(VATTN_EINVAL, "mha_dpsum: tensors must be 16-byte aligned");
+    if ((rc = check_device())) return rc;
+    const int BH = units(cfg), N = cfg->seq_len;
+    const long long rows = static_cast<long long>(BH) * N;
+    long long blocks = (rows + 15) / 16;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    const dim3 grid(static_cast<unsigned>(blocks));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // the backward's preprocess kernel with no padding and no lse2 output
+    if (cfg->head_dim == 128) {
+        if (cfg->dtype == VATTN_BF16)
+            launch_pdl(mha_bwd_preprocess_kernel<128, true>, grid, dim3(256), 0, s, o, dout, (const float*)nullptr,
+                       (float*)nullptr, d_rows, N, N, BH);
+        else
+            launch_pdl(mha_bwd_preprocess_kernel<128, false>, grid, dim3(256), 0, s, o, dout, (const float*)nullptr,
+                       (float*)nullptr, d_rows, N, N, BH);
+    } else {
+        if (cfg->dtype == VATTN_BF16)
+            launch_pdl(mha_bwd_preprocess_kernel<64, true>, grid, dim3(256), 0, s, o, dout, (const float*)nullptr,
+                       (float*)nullptr, d_rows, N, N, BH);
+        else
+            launch_pdl(mha_bwd_preprocess_kernel<64, false>, grid, dim3(256), 0, s, o, dout, (const float*)nullptr,
+                       (float*)nullptr, d_rows, N, N, BH);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = g_launch_err;
+    g_launch_err = cudaSuccess;
+    if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("mha_dpsum launch: ") + cudaGetErrorString(e));
+    g_launches = 1;
+    return VATTN_OK;
+}
+
+int vattn_dropout_digest(const vattn_config* cfg, int tile_rows, int tile_cols, unsigned long long* digest,
+                         void* stream) {
+    g_launches = 0;
+    int rc = validate(cfg);
+    if (rc) return rc;
+    if (!digest) return fail(VATTN_EINVAL, "vattn_dropout_digest: null pointer");
+    if (tile_rows < 1 || tile_cols < 1) return fail(VATTN_EINVAL, "vattn_dropout_digest: tiles must be positive");
+    if ((rc = check_device())) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(digest, 0, sizeof(unsigned long long), s) != cudaSuccess)
+        return fail(VATTN_ECUDA, "vattn_dropout_digest: memset");
+    if (cfg->dropout_p <= 0.0f) return VATTN_OK;  // no mask consumed: digest 0 (as the reference)
+    int H, bh_off;
+    float inv_keep;
+    uint64_t seed, thresh;
+    set_dropout(cfg, &H, &bh_off, &inv_keep, &seed, &thresh);
+    const int N = cfg->seq_len;
+    const dim3 grid((N + tile_rows - 1) / tile_rows, units(cfg));
+    dropout_digest_kernel<<<grid, 256, 0, s>>>(digest, seed, H, bh_off, N, tile_rows, tile_cols, cfg->causal, thresh);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("vattn_dropout_digest: ") + cudaGetErrorString(e));
+    g_launches = 1;
+    return VATTN_OK;
 }
 
 size_t mha_backward_workspace_bytes(const vattn_config* cfg) {

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) mha_bwd_preprocess_kernel(
         for (int off = kLanesPerRow / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
         if (sub == 0 && row < rows) {
             dsum[row] = valid ? acc : 0.0f;
-            lse2[row] = valid ? lse[static_cast<size_t>(bh) * N + n] * 1.4426950408889634f : INFINITY;
+            if (lse2) lse2[row] = valid ? lse[static_cast<size_t>(bh) * N + n] * 1.4426950408889634f : INFINITY;
         }
     }
     griddep_launch_dependents();

@@ -93,7 +93,7 @@ int check(const vattn_config* c) {
     if (!c) return fail(VATTN_EINVAL, "vattn_config: null");
     if (c->batch < 1 || c->heads < 1 || c->seq_len < 1 || c->head_dim < 1)
         return fail(VATTN_EINVAL, "AttnConfig: sizes must be positive");
-    if (c->head_dim % 8 != 0) return fail(VATTN_EUNSUPPORTED, "traditional: head_dim must be a multiple of 8");
+    if (c->head_dim % 4 != 0) return fail(VATTN_EINVAL, "AttnConfig: head_dim must be a multiple of 4");
     if (c->dtype != VATTN_F16 && c->dtype != VATTN_BF16) return fail(VATTN_EINVAL, "vattn_config: dtype");
     if (!(c->dropout_p >= 0.0f && c->dropout_p < 1.0f))
         return fail(VATTN_EINVAL, "AttnConfig: dropout_p must be in [0, 1)");

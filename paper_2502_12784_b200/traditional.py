@@ -37,7 +37,7 @@ def workspace_bytes(q: torch.Tensor, causal: bool = False) -> int:
 
 def forward_traditional(q, k, v, causal: bool = False, softmax_scale: float = 0.0, dropout_p: float = 0.0,
                         seed: int = 0, workspace=None):
-    """Three-pass forward on CUDA tensors [B, H, N, d] (d % 8 == 0): returns (out, lse)."""
+    """Three-pass forward on CUDA tensors [B, H, N, d] (d % 4 == 0): returns (out, lse)."""
     _check((q, k, v), q.shape, q.dtype, ("q", "k", "v"))
     B, H, N, d = q.shape
     cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
