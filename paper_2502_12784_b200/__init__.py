@@ -32,7 +32,7 @@ import torch
 __all__ = [
     "AttnConfig", "forward_fused", "backward_fused", "mha_forward", "mha_backward",
     "workspace_bytes", "MHAFunction", "attention", "LIB_PATH", "lib",
-    "mha_forward_host", "mha_backward_host", "mha_step_host", "compute_dpsum",
+    "mha_forward_host", "mha_backward_host", "mha_step_host", "compute_dpsum", "dropout_digest",
 ]
 
 LIB_PATH = os.environ.get("VATTN_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvattn_b200.so")
@@ -68,6 +68,8 @@ def _load():
     lib.mha_backward_host.restype = C.c_int
     lib.mha_step_host.argtypes = [C.POINTER(_Cfg)] + [vp] * 10
     lib.mha_step_host.restype = C.c_int
+    lib.vattn_dropout_digest.argtypes = [C.POINTER(_Cfg), C.c_int, C.c_int, vp, vp]
+    lib.vattn_dropout_digest.restype = C.c_int
     lib.mha_dpsum.argtypes = [C.POINTER(_Cfg)] + [vp] * 4
     lib.mha_dpsum.restype = C.c_int
     lib.vattn_last_error.restype = C.c_char_p
@@ -304,6 +306,20 @@ def compute_dpsum(d_out, out):
     if rc:
         _raise(rc, "mha_dpsum")
     return D
+
+
+def dropout_digest(cfg: "AttnConfig", traditional: bool = False) -> int:
+    """The reference's ``mask_digest`` for ``cfg`` (its tile sizes decide the visited
+    positions; ``traditional`` = every N x N position), bit-identical to the
+    reference (C ABI ``vattn_dropout_digest``)."""
+    c = _Cfg(cfg.batch, cfg.heads, cfg.seq_len, _native_dim(cfg.head_dim), 0 if traditional else int(cfg.causal),
+             float(cfg.softmax_scale), VATTN_F16, float(cfg.dropout_p), int(cfg.seed), 0, 0)
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    br, bc = (cfg.seq_len, cfg.seq_len) if traditional else (cfg.tile_rows, cfg.tile_cols)
+    rc = lib.vattn_dropout_digest(C.byref(c), br, bc, out.data_ptr(), _stream())
+    if rc:
+        _raise(rc, "vattn_dropout_digest")
+    return int(out.item()) & ((1 << 64) - 1)
 
 
 # ----------------------------------------- reference-shaped operator API --

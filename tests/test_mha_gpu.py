@@ -317,3 +317,29 @@ def test_dq_modes_vs_binary64(mode):
     r = subprocess.run([sys.executable, "-c", _DQ_MODE_CHILD], env=dict(os.environ, VATTN_DQ_MODE=mode, ROOT=root),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+# --------------------------------------- compute_dpsum and the mask digest --
+
+@pytest.mark.parametrize("d,dtype", [(64, torch.float16), (128, torch.bfloat16)])
+def test_compute_dpsum_vs_torch(d, dtype):
+    """vattn::compute_dpsum (backward.hpp:43) through the C ABI mha_dpsum."""
+    o, do = (t for t in workload(3, (2, 3, 200, d), dtype)[:2])
+    D = vb.compute_dpsum(do, o)
+    ref = (do.double() * o.double()).sum(-1)
+    assert torch.allclose(D.double(), ref, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("N,br,bc,causal", [(64, 16, 16, False), (128, 64, 32, True), (96, 32, 16, True)])
+def test_dropout_digest_bitwise_vs_reference(N, br, bc, causal):
+    """mask_digest (attention.hpp:32) equals the reference library's own value."""
+    if not po.ref_available():
+        pytest.skip("reference library not built")
+    B, H, d, p, seed = 1, 2, 32, 0.25, 777
+    q16, k16, v16 = (po.normal16(5, s, (B, H, N, d)) for s in (1, 2, 3))
+    _, _, ref_digest = po.ref_forward_fused_dropout(q16, k16, v16, causal, p, seed, br=br, bc=bc)
+    cfg = vb.AttnConfig(batch=B, heads=H, seq_len=N, head_dim=d, tile_rows=br, tile_cols=bc, causal=causal,
+                        dropout_p=p, seed=seed)
+    assert vb.dropout_digest(cfg) == ref_digest
+    cfg0 = vb.AttnConfig(batch=B, heads=H, seq_len=N, head_dim=d, tile_rows=br, tile_cols=bc, causal=causal)
+    assert vb.dropout_digest(cfg0) == 0
