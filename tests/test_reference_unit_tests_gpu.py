@@ -42,3 +42,27 @@ def test_reference_unit_tests_against_b200_path():
     assert not unexpected, f"reference tests failing on the B200 path: {unexpected}\n{out[-4000:]}"
     passed = sum(results.values())
     assert passed >= len(results) - len(EXPECTED_FAIL), out[-2000:]
+
+
+ACC_BIN = os.path.join(os.path.dirname(__file__), "refsuite", "_build", "ref_acceptance")
+# criterion 2 (forward mean_rel <= 0.1 %) fails for the reference itself (proj/test_output.txt:
+# 0.167 %; the metric is ill-conditioned near zero outputs) and at the same level
+# here; criterion 8 reads the emulated-Volta mma_invocations counter (reported as 0 on B200).
+ACC_EXPECTED_FAIL = {2, 8}
+
+
+def test_reference_acceptance_suite_against_b200_path():
+    """proj/tests/acceptance.cpp (criteria 1-10) on the B200 path: 8/10, including
+    criterion 3 (backward accuracy) that the reference's own FP16-ACC backward fails."""
+    if not os.path.exists(ACC_BIN):
+        pytest.skip("tests/refsuite not built")
+    out = subprocess.run([ACC_BIN], capture_output=True, text=True, timeout=900).stdout
+    crit = {}
+    for line in out.splitlines():
+        if line.startswith("[PASS] criterion") or line.startswith("[FAIL] criterion"):
+            n = int(line.split("criterion")[1].split(":")[0])
+            crit[n] = line.startswith("[PASS]")
+    assert sorted(crit) == list(range(1, 11)), out[-3000:]
+    bad = [n for n, ok in crit.items() if not ok and n not in ACC_EXPECTED_FAIL]
+    assert not bad, out
+    assert crit[3], "backward accuracy criterion must pass on the fp32-accumulating GPU path"
