@@ -43,7 +43,10 @@ template <int kD>
 struct FwdCfg {
     static constexpr int kTileBytes = kD * 128 * 2;     // one 128-row 16-bit tile
     static constexpr int kBoxes = kD / 64;              // 64-column TMA boxes per tile
-    static constexpr int kStages = kD == 128 ? 4 : 8;   // K/V ring depth
+#ifndef VATTN_FWD_STAGES128
+#define VATTN_FWD_STAGES128 4
+#endif
+    static constexpr int kStages = kD == 128 ? VATTN_FWD_STAGES128 : 8;   // K/V ring depth
     static constexpr int kSmemQ = 0;                    // Q0, Q1
     static constexpr int kSmemKV = 2 * kTileBytes;
     static constexpr int kSmemBar = kSmemKV + kStages * kTileBytes;

@@ -1,0 +1,51 @@
+"""GPU: BASELINE.json's full-size configs (SURVEY 8c "large configs").  The binary64
+oracle cannot run at these sizes, so each config is checked by properties that hold at
+any size -- bitwise run-to-run determinism of O, lse, dQ, dK, dV -- and by sampled
+(b, h) slices against a torch fp32 reference of the same slice on the GPU (same
+tolerances as the parity tests, relaxed 2x on fro for the long fp32 reference sums)."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2502_12784_b200 as vb
+    from tests.gpu_util import check_close, check_lse, torch_ref_grads, widen
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+FULL = [
+    # name, shape, causal, dtype, sampled (b, h) slices
+    ("C3", (4, 16, 8192, 128), True, torch.bfloat16, [(0, 0), (3, 15)]),
+    ("C2 N=16k", (1, 32, 16384, 64), False, torch.float16, [(0, 7)]),
+    ("C5 one GPU", (1, 64, 32768, 128), True, torch.bfloat16, [(0, 63)]),
+]
+
+
+@pytest.mark.parametrize("name,shape,causal,dtype,samples", FULL, ids=[f[0] for f in FULL])
+def test_full_size_determinism_and_sampled_parity(name, shape, causal, dtype, samples):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(2026)
+    q, k, v, do = (torch.randn(shape, generator=g, device="cuda").to(dtype) for _ in range(4))
+    o, lse = vb.mha_forward(q, k, v, causal)
+    dq, dk, dv = vb.mha_backward(q, k, v, o, do, lse, causal)
+    o2, lse2 = vb.mha_forward(q, k, v, causal)
+    g2 = vb.mha_backward(q, k, v, o2, do, lse2, causal)
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2) and torch.equal(lse, lse2)
+    for a, b in zip((dq, dk, dv), g2):
+        assert torch.equal(a, b)
+    for b_, h_ in samples:
+        sl = (slice(b_, b_ + 1), slice(h_, h_ + 1))
+        ro, rlse, rdq, rdk, rdv = torch_ref_grads(q[sl], k[sl], v[sl], do[sl], causal)
+        for nm, t, r in (("O", o, ro), ("dQ", dq, rdq), ("dK", dk, rdk), ("dV", dv, rdv)):
+            check_close(widen(t[sl]), r.double().cpu().numpy(), dtype, f"{name} {nm} (b={b_},h={h_})",
+                        fro=2e-3 if dtype == torch.float16 else 1.6e-2)
+        check_lse(lse[sl].cpu().double().numpy(), rlse.double().cpu().numpy(), max_rel=2e-5)
+        del ro, rlse, rdq, rdk, rdv
+        torch.cuda.empty_cache()
