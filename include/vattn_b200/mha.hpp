@@ -37,6 +37,10 @@
 
 namespace vattn_b200 {
 
+// vattn::AccMode (attention.hpp:9).  Selects the reference's emulated softmax-stage
+// datapath, so it only changes the reported event counters; the GPU accumulates in fp32.
+enum class AccMode { FP16_ACC, FP32_ACC };
+
 struct AttnConfig {
     int batch = 1;
     int heads = 1;
@@ -49,6 +53,7 @@ struct AttnConfig {
     uint64_t seed = 0;
     float softmax_scale = 0.0f;  // <= 0 picks 1/sqrt(head_dim)
     vattn_dtype dtype = VATTN_F16;
+    AccMode acc_mode = AccMode::FP32_ACC;
 
     // AttnConfig::validate (proj/src/attention_forward.cpp:31-40), minus the
     // N % tile requirement the GPU path does not need.
@@ -77,8 +82,9 @@ struct AttnConfig {
 // nothing, so the reference's modeled-HBM counters are filled from closed forms of
 // its own bookkeeping (traffic_* below; pinned to the reference library by
 // tests/test_traffic_spat.py and tests/cpp/mha_cpp_parity.cpp).  The Volta
-// datapath events (mma_invocations, shuffle_events, convert_events) have no B200
-// counterpart and stay 0; measured DRAM bytes are in profiles/.
+// datapath events (mma_invocations, shuffle_events, convert_events) are pure
+// functions of the config too and are restated the same way (paper_2502_12784_b200/
+// traffic.py documents each term); measured DRAM bytes are in profiles/.
 struct TrafficCounter {
     uint64_t matrix_pass_reads = 0;
     uint64_t matrix_pass_writes = 0;
@@ -116,24 +122,62 @@ inline uint64_t visited_pairs(const AttnConfig& c) {
     return t;
 }
 
+// m8n8k4 invocations of one tile GEMM C[rows x cols] += A[rows x k] B[k x cols]
+// (tile_pipeline.cpp:36-49): (k/4) k-steps x rows/8 bands x ceil(cols/32) chunks.
+inline uint64_t mma_count(uint64_t rows, uint64_t cols, uint64_t k) {
+    return (k / 4) * (rows / 8) * ((cols / 8 + 3) / 4);
+}
+inline uint64_t pad8(uint64_t d) { return (d + 7) / 8 * 8; }
+
+// Per-(b,h) events of T visited forward pairs (attention_forward.cpp:126-173).
+inline void forward_events(uint64_t br, uint64_t bc, uint64_t d, uint64_t T, bool fp16_acc, uint64_t& mma,
+                           uint64_t& shf, uint64_t& cvt) {
+    mma = T * (mma_count(br, bc, d) + mma_count(br, pad8(d), bc));
+    shf = fp16_acc ? 0 : T * 2 * (br / 8);        // xor rounds for row max and row sum
+    cvt = fp16_acc ? T * (2 * br * bc + 2 * br * d) : 0;  // S widened, O round trip, P narrowed
+}
+
 inline TrafficCounter traffic_forward_fused(const AttnConfig& c) {
     const uint64_t BH = static_cast<uint64_t>(c.batch) * c.heads, N = c.seq_len, d = c.head_dim;
+    const uint64_t T = visited_pairs(c);
     TrafficCounter t;
     t.matrix_pass_reads = 3;  // Q, K, V
     t.matrix_pass_writes = 1;  // O
-    t.element_reads = BH * (N * d + 2ull * c.tile_cols * d * visited_pairs(c));
+    t.element_reads = BH * (N * d + 2ull * c.tile_cols * d * T);
     t.element_writes = BH * (N * d + N);
+    uint64_t mma, shf, cvt;
+    forward_events(c.tile_rows, c.tile_cols, d, T, c.acc_mode == AccMode::FP16_ACC, mma, shf, cvt);
+    t.mma_invocations = BH * mma;
+    t.shuffle_events = BH * shf;
+    t.convert_events = BH * cvt;
+    return t;
+}
+
+// forward_traditional (attention_forward.cpp:229-310): S, P materialised, 5/3 passes.
+inline TrafficCounter traffic_forward_traditional(const AttnConfig& c) {
+    const uint64_t BH = static_cast<uint64_t>(c.batch) * c.heads, N = c.seq_len, d = c.head_dim;
+    TrafficCounter t;
+    t.matrix_pass_reads = 5;   // Q, K | S | P, V
+    t.matrix_pass_writes = 3;  // S | P | O
+    t.element_reads = BH * (3 * N * d + 2 * N * N);
+    t.element_writes = BH * (2 * N * N + N * d + N);
+    t.mma_invocations = BH * (mma_count(N, N, d) + mma_count(N, pad8(d), N));
     return t;
 }
 
 inline TrafficCounter traffic_backward_fused(const AttnConfig& c) {
     const uint64_t BH = static_cast<uint64_t>(c.batch) * c.heads, N = c.seq_len, d = c.head_dim;
-    const uint64_t br = c.tile_rows, bc = c.tile_cols, T = visited_pairs(c), nk = N / bc;
+    const uint64_t br = c.tile_rows, bc = c.tile_cols, T = visited_pairs(c), nk = N / bc, dp = pad8(d);
     TrafficCounter t;
     t.matrix_pass_reads = 10;  // pre-pass Q K V; Q K V dO lse D; dQ finalize read
     t.matrix_pass_writes = 5;  // D, dK, dV, dQ adds, dQ narrowing
     t.element_reads = BH * ((N * d + 2 * bc * d * T) + 2 * bc * d * nk + T * (2 * br * d + 2 * br) + N * d);
     t.element_writes = BH * (N + T * br * d + 2 * bc * d * nk + N * d);
+    uint64_t mma, shf, cvt;
+    forward_events(br, bc, d, T, true, mma, shf, cvt);  // FP16-ACC recompute pre-pass (attention_backward.cpp:93-103)
+    // S, dV, dP, dQ, dK GEMMs and four Br x Bc conversions per visited pair (:132-199)
+    t.mma_invocations = BH * (mma + T * (2 * mma_count(br, bc, d) + 2 * mma_count(bc, dp, br) + mma_count(br, dp, bc)));
+    t.convert_events = BH * (cvt + T * 4 * br * bc);
     return t;
 }
 

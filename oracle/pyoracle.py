@@ -311,3 +311,14 @@ def ref_attention_grad_ref_dropout(q, k, v, dout, causal, dropout_p, seed, scale
     assert ref_lib().vr_attention_grad_ref_dropout(B, H, N, d, int(causal), scale, dropout_p, seed, c(q), c(k),
                                                    c(v), c(dout), dq, dk, dv) == 0
     return dq, dk, dv
+
+
+def ref_traffic_counts(which, B, H, N, d, br, bc, causal):
+    """The reference library's TrafficCounter (7 fields) for a generated workload
+    (ref_shim.cpp vr_traffic: 0/3 forward_fused FP32/FP16-ACC, 1/4 forward_traditional
+    FP32/FP16-ACC, 2 backward_fused)."""
+    out = (C.c_uint64 * 7)()
+    rc = ref_lib().vr_traffic(which, B, H, N, d, br, bc, int(causal), out)
+    if rc:
+        raise RuntimeError(ref_lib().vr_last_error().decode())
+    return tuple(out)

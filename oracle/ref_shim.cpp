@@ -299,10 +299,13 @@ int vr_traffic(int which, int B, int H, int N, int d, int br, int bc, int causal
         const auto dims = dims4(B, H, N, d);
         const Tensor<Half> q = normal_tensor_f16(1, 1, dims), k = normal_tensor_f16(1, 2, dims),
                            v = normal_tensor_f16(1, 3, dims), dout = normal_tensor_f16(1, 4, dims);
-        if (which == 0) {  // forward_fused, FP32-ACC
-            put_traffic(forward_fused(q, k, v, make_cfg(B, H, N, d, br, bc, causal, 0, 0.0f)).traffic, out);
-        } else if (which == 1) {  // forward_traditional, FP32-ACC
-            put_traffic(forward_traditional(q, k, v, make_cfg(B, H, N, d, br, bc, causal, 0, 0.0f)).traffic, out);
+        // which: 0 forward_fused FP32-ACC, 1 forward_traditional FP32-ACC, 2 backward_fused,
+        //        3 forward_fused FP16-ACC, 4 forward_traditional FP16-ACC
+        if (which == 0 || which == 3) {
+            put_traffic(forward_fused(q, k, v, make_cfg(B, H, N, d, br, bc, causal, which == 3, 0.0f)).traffic, out);
+        } else if (which == 1 || which == 4) {
+            put_traffic(forward_traditional(q, k, v, make_cfg(B, H, N, d, br, bc, causal, which == 4, 0.0f)).traffic,
+                        out);
         } else {  // backward_fused (FP16-ACC, its only mode)
             const AttnConfig c = make_cfg(B, H, N, d, br, bc, causal, 1, 0.0f);
             const ForwardOutput f = forward_fused(q, k, v, c);

@@ -106,6 +106,7 @@ class AttnConfig:
     dropout_p: float = 0.0
     seed: int = 0
     softmax_scale: float = 0.0
+    acc_mode: str = "fp32"  # AccMode (attention.hpp:9): reported in traffic/report only; the GPU accumulates in fp32
 
     def validate(self, strict_tiles: bool = True) -> None:
         """AttnConfig::validate (attention_forward.cpp:31-40).  ``strict_tiles=False``
@@ -122,6 +123,7 @@ class AttnConfig:
             req(self.seq_len % self.tile_rows == 0, "AttnConfig: seq_len must be a multiple of tile_rows")
             req(self.seq_len % self.tile_cols == 0, "AttnConfig: seq_len must be a multiple of tile_cols")
         req(0.0 <= self.dropout_p < 1.0, "AttnConfig: dropout_p must be in [0, 1)")
+        req(str(self.acc_mode).lower() in ("fp16", "fp32"), "AttnConfig: acc_mode must be fp16 or fp32")
 
     def scale(self) -> float:
         """AttnConfig::scale (attention_forward.cpp:42-45), binary32."""

@@ -18,9 +18,23 @@ the operator API; tests pin them to the reference library's counters.
   atomic add (Br d) written, dK, dV stored (2 Bc d), and the dQ finalisation
   (N d read + N d written).
 
-``mma_invocations``, ``shuffle_events`` and ``convert_events`` count Volta
-m8n8k4 / warp-shuffle / fp16<->fp32 conversion events of the emulated datapath,
-which has no counterpart on Blackwell (out of scope); they are 0 here.
+``mma_invocations``, ``shuffle_events`` and ``convert_events`` count the events
+of the reference's emulated Volta datapath.  The B200 kernels do not execute that
+datapath, but the counts are pure functions of the config, so they are restated
+too (the reports of ``reports.py`` then equal the reference's field for field):
+
+* one m8n8k4 invocation per (k-step of 4, 8-row band, chunk of four 8-column
+  sub-tiles) of a tile GEMM C[rows x cols] += A[rows x k] B[k x cols]
+  (tile_pipeline.cpp:36-49, tile_pipeline.hpp:24-33): (k/4)(rows/8)ceil(cols/32);
+  P.V and dS.K run on the head dim padded to 8 (``pad8``);
+* forward, per visited pair: S = Q K^T and O += P V; FP32-ACC adds 2 Br/8 xor
+  shuffle rounds (attention_forward.cpp:147-148), FP16-ACC converts S, O (twice)
+  and P (:136-137, :151-152, :164-165);
+* backward (FP16-ACC only), per visited pair: S, dV, dP, dQ, dK GEMMs and four
+  Br Bc conversions (attention_backward.cpp:132-199), on top of the FP16-ACC
+  forward pre-pass (:93-103);
+* traditional: S = Q K^T and O = P V on the whole N x N tile, no events
+  (attention_forward.cpp:253-300).
 Measured DRAM bytes of the B200 kernels are in profiles/*_ncu_full_*.md.
 """
 from __future__ import annotations
@@ -60,15 +74,39 @@ def _dims(cfg):
     return cfg.batch * cfg.heads, cfg.seq_len, cfg.head_dim, cfg.tile_rows, cfg.tile_cols, bool(cfg.causal)
 
 
+def _fp16_acc(cfg) -> bool:
+    return str(getattr(cfg, "acc_mode", "fp32")).lower() in ("fp16", "fp16_acc")
+
+
+def pad8(d: int) -> int:
+    """detail::pad8: head dim rounded up to a multiple of 8."""
+    return (d + 7) // 8 * 8
+
+
+def mma_count(rows: int, cols: int, k: int) -> int:
+    """m8n8k4 invocations of one tile GEMM (tile_pipeline.cpp:36-49)."""
+    return (k // 4) * (rows // 8) * ((cols // 8 + 3) // 4)
+
+
+def _forward_events(br, bc, d, T, fp16_acc):
+    """(mma, shuffles, converts) of T visited forward pairs (attention_forward.cpp:126-173)."""
+    mma = T * (mma_count(br, bc, d) + mma_count(br, pad8(d), bc))
+    if fp16_acc:
+        return mma, 0, T * (2 * br * bc + 2 * br * d)
+    return mma, T * 2 * (br // 8), 0
+
+
 def forward_fused_traffic(cfg) -> TrafficCounter:
     BH, N, d, br, bc, causal = _dims(cfg)
     T = visited_pairs(N, br, bc, causal)
-    return TrafficCounter(3, 1, BH * (N * d + 2 * bc * d * T), BH * (N * d + N))
+    mma, shf, cvt = _forward_events(br, bc, d, T, _fp16_acc(cfg))
+    return TrafficCounter(3, 1, BH * (N * d + 2 * bc * d * T), BH * (N * d + N), BH * mma, BH * shf, BH * cvt)
 
 
 def forward_traditional_traffic(cfg) -> TrafficCounter:
     BH, N, d, _, _, _ = _dims(cfg)
-    return TrafficCounter(5, 3, BH * (3 * N * d + 2 * N * N), BH * (2 * N * N + N * d + N))
+    mma = mma_count(N, N, d) + mma_count(N, pad8(d), N)
+    return TrafficCounter(5, 3, BH * (3 * N * d + 2 * N * N), BH * (2 * N * N + N * d + N), BH * mma)
 
 
 def backward_fused_traffic(cfg) -> TrafficCounter:
@@ -77,4 +115,8 @@ def backward_fused_traffic(cfg) -> TrafficCounter:
     nk = N // bc
     reads = (N * d + 2 * bc * d * T) + 2 * bc * d * nk + T * (2 * br * d + 2 * br) + N * d
     writes = N + T * br * d + 2 * bc * d * nk + N * d
-    return TrafficCounter(10, 5, BH * reads, BH * writes)
+    pre_mma, _, pre_cvt = _forward_events(br, bc, d, T, True)  # the FP16-ACC recompute pre-pass
+    dp = pad8(d)
+    mma = pre_mma + T * (2 * mma_count(br, bc, d) + 2 * mma_count(bc, dp, br) + mma_count(br, dp, bc))
+    cvt = pre_cvt + T * 4 * br * bc
+    return TrafficCounter(10, 5, BH * reads, BH * writes, BH * mma, 0, BH * cvt)

@@ -59,6 +59,7 @@ vattn_b200::AttnConfig to_b200(const AttnConfig& c) {
     b.seed = c.seed;
     b.softmax_scale = c.softmax_scale;
     b.dtype = VATTN_F16;
+    b.acc_mode = c.acc_mode == AccMode::FP16_ACC ? vattn_b200::AccMode::FP16_ACC : vattn_b200::AccMode::FP32_ACC;
     return b;
 }
 
@@ -80,6 +81,9 @@ TrafficCounter to_ref(const vattn_b200::TrafficCounter& b) {
     t.matrix_pass_writes = b.matrix_pass_writes;
     t.element_reads = b.element_reads;
     t.element_writes = b.element_writes;
+    t.mma_invocations = b.mma_invocations;
+    t.shuffle_events = b.shuffle_events;
+    t.convert_events = b.convert_events;
     return t;
 }
 
@@ -161,11 +165,7 @@ ForwardOutput forward_traditional(const Tensor<Half>& q, const Tensor<Half>& k, 
     }
     for (void* p : {dq, dk, dv, dout, dlse, ws}) cudaFree(p);
     if (rc != VATTN_OK) throw std::invalid_argument(vattn_traditional_last_error());
-    const std::size_t BH = static_cast<std::size_t>(cfg.batch) * cfg.heads, N = cfg.seq_len, d = cfg.head_dim;
-    out.traffic.matrix_pass_reads = 5;
-    out.traffic.matrix_pass_writes = 3;
-    out.traffic.element_reads = BH * (3 * N * d + 2 * N * N);
-    out.traffic.element_writes = BH * (2 * N * N + N * d + N);
+    out.traffic = to_ref(vattn_b200::traffic_forward_traditional(to_b200(cfg)));
     vattn_config all = c;  // the traditional pass consumes every N x N position
     all.causal = 0;
     out.mask_digest = vattn_b200::detail::mask_digest(all, cfg.seq_len, cfg.seq_len);

@@ -16,10 +16,6 @@ EXPECTED_FAIL = {
     # bit-for-bit equality with the emulated Volta m8n8k4 pipeline (tensor cores
     # accumulate in a different order: parity is tolerance-based)
     "single tile degenerate case equals the dense one-shot MMA pipeline bit for bit",
-    # counters of the emulated Volta datapath (mma_invocations, shuffle/convert
-    # events) -- no Blackwell counterpart, reported as 0
-    "causal halves the MMA work within tile slack",
-    "softmax-stage counters expose the FP16/FP32 trade-off",
     # the GPU backward always accumulates in fp32, so FP32-ACC is accepted
     "FP32-ACC backward is rejected as unsupported",
     # emulation inspection hooks (ForwardTrace, DqContribution log) are not produced
@@ -47,12 +43,12 @@ def test_reference_unit_tests_against_b200_path():
 ACC_BIN = os.path.join(os.path.dirname(__file__), "refsuite", "_build", "ref_acceptance")
 # criterion 2 (forward mean_rel <= 0.1 %) fails for the reference itself (proj/test_output.txt:
 # 0.167 %; the metric is ill-conditioned near zero outputs) and at the same level
-# here; criterion 8 reads the emulated-Volta mma_invocations counter (reported as 0 on B200).
-ACC_EXPECTED_FAIL = {2, 8}
+# here.  Criterion 8 (causal mma_invocations) passes through the closed-form counters.
+ACC_EXPECTED_FAIL = {2}
 
 
 def test_reference_acceptance_suite_against_b200_path():
-    """proj/tests/acceptance.cpp (criteria 1-10) on the B200 path: 8/10, including
+    """proj/tests/acceptance.cpp (criteria 1-10) on the B200 path: 9/10, including
     criterion 3 (backward accuracy) that the reference's own FP16-ACC backward fails."""
     if not os.path.exists(ACC_BIN):
         pytest.skip("tests/refsuite not built")

@@ -22,21 +22,22 @@ def ref_traffic(which, B, H, N, d, br, bc, causal):
 
 
 CASES = [(1, 1, 64, 32, 16, 16, False), (1, 1, 64, 32, 16, 16, True), (2, 3, 128, 64, 64, 32, True),
-         (1, 2, 96, 16, 32, 16, True), (1, 2, 96, 16, 16, 32, False), (2, 1, 64, 8, 64, 64, True)]
+         (1, 2, 96, 16, 32, 16, True), (1, 2, 96, 16, 16, 32, False), (2, 1, 64, 8, 64, 64, True),
+         (1, 1, 80, 12, 16, 40, True), (1, 2, 120, 20, 40, 24, False)]  # d not a multiple of 8, odd chunks
 
 
 @need_ref
 @pytest.mark.parametrize("B,H,N,d,br,bc,causal", CASES)
 def test_traffic_closed_forms_match_reference(B, H, N, d, br, bc, causal):
-    cfg = AttnConfig(batch=B, heads=H, seq_len=N, head_dim=d, tile_rows=br, tile_cols=bc, causal=causal)
-    for which, fn in ((0, tf.forward_fused_traffic), (1, tf.forward_traditional_traffic),
-                      (2, tf.backward_fused_traffic)):
-        ref = ref_traffic(which, B, H, N, d, br, bc, causal)
-        ours = fn(cfg).as_tuple()
-        # pass counts and element traffic are restated exactly; the Volta event
-        # counters (mma / shuffle / convert) are not modeled on B200
-        assert ours[:4] == ref[:4], (which, ours, ref)
-        assert ours[4:] == (0, 0, 0)
+    """All seven counters, both accumulation modes, equal the reference library's."""
+    for acc, cases in (("fp32", ((0, tf.forward_fused_traffic), (1, tf.forward_traditional_traffic))),
+                       ("fp16", ((3, tf.forward_fused_traffic), (4, tf.forward_traditional_traffic),
+                                 (2, tf.backward_fused_traffic)))):
+        cfg = AttnConfig(batch=B, heads=H, seq_len=N, head_dim=d, tile_rows=br, tile_cols=bc, causal=causal,
+                         acc_mode=acc)
+        for which, fn in cases:
+            ref = ref_traffic(which, B, H, N, d, br, bc, causal)
+            assert fn(cfg).as_tuple() == ref, (which, acc, fn(cfg).as_tuple(), ref)
 
 
 def test_traffic_causal_halves_visits():
