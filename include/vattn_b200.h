@@ -155,6 +155,7 @@ int vattn_last_launch_count(void);
 #define VATTN_KERNEL_FWD 0     /* fused forward                      */
 #define VATTN_KERNEL_BWD_DKDV 1 /* backward, key-major dK / dV kernel */
 #define VATTN_KERNEL_BWD_DQ 2   /* backward, query-major dQ kernel    */
+#define VATTN_KERNEL_BWD_PRE 3  /* backward preprocess (D, lse2)      */
 void vattn_profile_enable(int on);
 int vattn_profile_read(int kind, double* ms_total, int* launches);
 

@@ -30,7 +30,7 @@ thread_local int g_launches = 0;
 // ---- measurement hooks (vattn_profile_*): event pairs around the hot kernels
 struct ProfPair {
     cudaEvent_t a, b;
-    int kind;  // 0 fwd, 1 bwd main
+    int kind;  // VATTN_KERNEL_* (include/vattn_b200.h)
 };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
@@ -312,6 +312,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const long long rows = static_cast<long long>(BH) * L.Npad;
         long long blocks = (rows + 7) / 8;
         if (blocks > 148 * 16) blocks = 148 * 16;
+        ProfScope prof(stream, 3);
         launch_pdl(mha_bwd_preprocess_kernel<kD, kBF16>, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream,
                    o, dout, lse, lse2, dsum, N, L.Npad, BH);
     }
