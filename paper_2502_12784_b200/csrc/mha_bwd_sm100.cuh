@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(384, 1)
                         const __grid_constant__ CUtensorMap tm_do,
                         const __grid_constant__ CUtensorMap tm_ds, void* __restrict__ dk_out,
                         void* __restrict__ dv_out, const BwdParams p) {
+    VCTA(1, 0);
     using Cfg = DkdvCfg<kD>;
     constexpr int kVtraceKid = 1;
     (void)kVtraceKid;
@@ -168,9 +169,9 @@ __global__ void __launch_bounds__(384, 1)
 
     const int warp = warp_id();
     const int lane = lane_id();
-    const int bh = grid_bh();
+    const int bh = grid_bh(p.n_q);
     // causal: the key tiles with the most query tiles first
-    const int kb = grid_tile();
+    const int kb = grid_tile(p.n_q);
     const int N = p.N;
     const int i0 = p.causal ? kb : 0;
     const int n_steps = p.n_q - i0;
@@ -480,6 +481,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         tmem_dealloc<512>(tmem);
     }
+    VCTA(1, 1);
 }
 
 // ===================================================================== dQ ==
@@ -519,6 +521,7 @@ __global__ void __launch_bounds__(384, 1)
                       const __grid_constant__ CUtensorMap tm_v,
                       const __grid_constant__ CUtensorMap tm_do,
                       const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
+    VCTA(2, 0);
     using Cfg = DqCfg<kD>;
     constexpr int kVtraceKid = 2;
     (void)kVtraceKid;
@@ -543,9 +546,9 @@ __global__ void __launch_bounds__(384, 1)
 
     const int warp = warp_id();
     const int lane = lane_id();
-    const int bh = grid_bh();
-    const int nqb = grid_ntiles();
-    const int i = p.causal ? (nqb - 1 - grid_tile()) : grid_tile();
+    const int nqb = p.n_q;
+    const int bh = grid_bh(nqb);
+    const int i = p.causal ? (nqb - 1 - grid_tile(nqb)) : grid_tile(nqb);
     const int N = p.N;
     const int nk = p.causal ? i + 1 : p.n_q;
 
@@ -806,6 +809,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         tmem_dealloc<512>(tmem);
     }
+    VCTA(2, 1);
 }
 
 // ============================================================ dQ = dS K ==
@@ -831,6 +835,7 @@ template <int kD, bool kBF16>
 __global__ void __launch_bounds__(256, 1)
     mha_bwd_dq_gemm_kernel(const __grid_constant__ CUtensorMap tm_ds, const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
+    VCTA(3, 0);
     using Cfg = DqGemmCfg<kD>;
     constexpr int S = Cfg::kStages;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -841,9 +846,9 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
     const int warp = warp_id();
     const int lane = lane_id();
-    const int bh = grid_bh();
-    const int nqb = grid_ntiles();
-    const int i = p.causal ? (nqb - 1 - grid_tile()) : grid_tile();
+    const int nqb = p.n_q;
+    const int bh = grid_bh(nqb);
+    const int i = p.causal ? (nqb - 1 - grid_tile(nqb)) : grid_tile(nqb);
     const int nk = p.causal ? i + 1 : p.n_q;
     if (threadIdx.x == 0) {
         if ((smem_u32(smem) & 1023u) != 0) __trap();
@@ -932,6 +937,7 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
         tmem_dealloc<kD>(tmem);
     }
+    VCTA(3, 1);
 }
 
 }  // namespace vattn_sm100

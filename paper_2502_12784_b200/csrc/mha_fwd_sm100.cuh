@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(384, 1)
                          const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v,
                          const __grid_constant__ CUtensorMap tm_o, const FwdParams p) {
+    VCTA(0, 0);
     using Cfg = FwdCfg<kD>;
     constexpr int kVtraceKid = 0;
     (void)kVtraceKid;
@@ -80,9 +81,9 @@ __global__ void __launch_bounds__(384, 1)
 
     const int warp = warp_id();
     const int lane = lane_id();
-    const int bh = grid_bh();
-    const int nqb = grid_ntiles();
-    const int qblk = p.causal ? (nqb - 1 - grid_tile()) : grid_tile();
+    const int nqb = (p.N + 255) / 256;
+    const int bh = grid_bh(nqb);
+    const int qblk = p.causal ? (nqb - 1 - grid_tile(nqb)) : grid_tile(nqb);
     const int q0 = qblk * 256;
     const int N = p.N;
 
@@ -395,6 +396,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         tmem_dealloc<512>(tmem);
     }
+    VCTA(0, 1);
 }
 
 }  // namespace vattn_sm100

@@ -27,13 +27,18 @@ VATTN_DEV uint32_t warp_id() { return threadIdx.x >> 5; }
 // tiles through L2 -- every kernel reads ~1.0x its algorithmic HBM bytes.  1: (b*h,
 // tile) on (x, y), longest causal item of every head first; measured on B200 it
 // loses that L2 sharing (C3 -10 %, C5 -22 %) and gains only ~3 % on short C4 heads.
-#ifndef VATTN_LPT_GRID
-#define VATTN_LPT_GRID 0
-#endif
-VATTN_DEV int grid_bh() { return VATTN_LPT_GRID ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.y); }
-VATTN_DEV int grid_tile() { return VATTN_LPT_GRID ? static_cast<int>(blockIdx.y) : static_cast<int>(blockIdx.x); }
-VATTN_DEV int grid_ntiles() { return VATTN_LPT_GRID ? static_cast<int>(gridDim.y) : static_cast<int>(gridDim.x); }
-inline dim3 tile_grid(int ntiles, int bh) { return VATTN_LPT_GRID ? dim3(bh, ntiles) : dim3(ntiles, bh); }
+// Block -> ((b,h) unit, tile).  The grid is (ntiles * G, BH / G): groups of G units
+// dispatch one after another, and inside a group the blocks go tile-major, so the
+// longest causal items of the group start first (longest-processing-time order) while
+// the group's shared streams (K/V in the forward, Q/dO in the backward) stay resident
+// in L2 across all of its tiles.  G = 1 is plain unit-major order (every unit's tiles
+// in a row); G = BH is global tile-major order.  Tile 0 is the heaviest causal item.
+VATTN_DEV int grid_tile(int ntiles) { return static_cast<int>(blockIdx.x) / (static_cast<int>(gridDim.x) / ntiles); }
+VATTN_DEV int grid_bh(int ntiles) {
+    const int G = static_cast<int>(gridDim.x) / ntiles;
+    return static_cast<int>(blockIdx.y) * G + static_cast<int>(blockIdx.x) % G;
+}
+inline dim3 tile_grid(int ntiles, int bh, int G) { return dim3(ntiles * G, bh / G); }
 VATTN_DEV uint32_t lane_id() { return threadIdx.x & 31; }
 
 // Per-warpgroup register budget hand-off (all 4 warps of the warpgroup execute it).
@@ -440,9 +445,33 @@ __device__ int g_vattn_trace_kid;  // which kernel (kVtraceKid of the kernel) is
             static_cast<int>(blockIdx.x + blockIdx.y * gridDim.x) == g_vattn_trace_block) \
             g_vattn_trace[(slot)] = clock64();                                           \
     } while (0)
+// Per-CTA timeline (which SM, globaltimer at entry and exit) of every CTA of the
+// kernel selected by g_vattn_trace_kid: the SM-busy fraction and the gaps between
+// consecutive CTAs on one SM (tools/cta_timeline.py).
+__device__ unsigned long long g_vattn_cta[16384][3];
+VATTN_DEV unsigned long long vcta_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define VCTA(kid, which)                                                                  \
+    do {                                                                                 \
+        const int b_ = static_cast<int>(blockIdx.x + blockIdx.y * gridDim.x);            \
+        if ((kid) == g_vattn_trace_kid && threadIdx.x == 0 && b_ < 16384) {               \
+            g_vattn_cta[b_][which] = vcta_now();                                          \
+            if ((which) == 0) {                                                          \
+                unsigned sm_;                                                            \
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                          \
+                g_vattn_cta[b_][2] = sm_;                                                \
+            }                                                                            \
+        }                                                                                \
+    } while (0)
 #else
 #define VTRACE(slot) \
     do {             \
+    } while (0)
+#define VCTA(kid, which) \
+    do {                 \
     } while (0)
 #endif
 
