@@ -208,6 +208,23 @@ int bh_group(int BH, long long per_unit_bytes, bool fwd) {
     return G;
 }
 
+// dK/dV dispatch (grid_item_tail): causal key tiles differ in length up to n_q-fold,
+// so the units of the last ~3.5 waves go longest-first (their heaviest tiles would
+// otherwise start in the final wave and leave a ~60 us per-SM tail at C3).  The rest
+// stays unit-major: all key tiles of one unit share its Q/dO stream in L2 (a fully
+// grouped order measured 3 % slower per CTA).  VATTN_DKDV_TAIL_WAVES overrides (0 = off).
+int dkdv_tail_units(int BH, int n_q) {
+    static const double waves = [] {
+        const char* e = getenv("VATTN_DKDV_TAIL_WAVES");
+        return e ? atof(e) : 3.5;
+    }();
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int T = static_cast<int>((waves * sms + n_q - 1) / n_q);
+    return T < 0 ? 0 : (T > BH ? BH : T);
+}
+
 // Launch with programmatic stream serialisation (see griddep_* in sm100_ptx.cuh):
 // the kernel's CTAs may start their prologue while the previous kernel drains.
 template <typename... Params, typename... Args>
@@ -352,6 +369,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     set_dropout(c, &p.H, &p.bh_off, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
     p.ds_out = L.materialize_ds ? reinterpret_cast<uint16_t*>(w + L.ds) : nullptr;
     p.ds_tiles_per_bh = L.ds_tiles_per_bh;
+    p.tail_units = c->causal ? dkdv_tail_units(BH, L.n_q) : 0;
     CUtensorMap mds;
     if (L.materialize_ds && !make_ds_map(&mds, p.ds_out, static_cast<long long>(BH) * L.ds_tiles_per_bh, kBF16))
         return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled (dS) failed");
@@ -362,8 +380,8 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
-        launch_pdl(kern, tile_grid(L.n_q, BH, bh_group(BH, 2ll * N * kD * 2, false)), dim3(384), smem, stream, mq, mk, mv, mdo,
-                   L.materialize_ds ? mds : mq, dk, dv, p);  // groups sized on Q, dO
+        launch_pdl(kern, dim3(L.n_q * BH), dim3(384), smem, stream, mq, mk, mv, mdo, L.materialize_ds ? mds : mq, dk, dv,
+                   p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)
     if (L.materialize_ds) {

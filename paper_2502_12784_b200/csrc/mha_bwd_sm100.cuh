@@ -88,6 +88,7 @@ struct BwdParams {
     // (mha_bwd_dq_gemm_kernel) instead of the recomputing dQ kernel.  nullptr = off.
     uint16_t* ds_out;
     long long ds_tiles_per_bh;  // n_q^2, or n_q (n_q + 1) / 2 causal (lower triangle)
+    int tail_units;             // dK/dV grid: last units dispatched longest-first (grid_item_tail)
 };
 
 // Index of dS^T tile (query tile i, key tile kb) within one (b, h).
@@ -169,9 +170,9 @@ __global__ void __launch_bounds__(384, 1)
 
     const int warp = warp_id();
     const int lane = lane_id();
-    const int bh = grid_bh(p.n_q);
     // causal: the key tiles with the most query tiles first
-    const int kb = grid_tile(p.n_q);
+    int bh, kb;
+    grid_item_tail(p.n_q, p.tail_units, bh, kb);
     const int N = p.N;
     const int i0 = p.causal ? kb : 0;
     const int n_steps = p.n_q - i0;

@@ -39,6 +39,22 @@ VATTN_DEV int grid_bh(int ntiles) {
     return static_cast<int>(blockIdx.y) * G + static_cast<int>(blockIdx.x) % G;
 }
 inline dim3 tile_grid(int ntiles, int bh, int G) { return dim3(ntiles * G, bh / G); }
+// 1-D variant with a longest-first tail: units [0, BH - T) unit-major, then the last T
+// units tile-major, so the heaviest causal items of the final units start waves before
+// the end instead of in the last wave (grid = ntiles * BH blocks along x).
+VATTN_DEV void grid_item_tail(int ntiles, int T, int& bh, int& tile) {
+    const int BH = static_cast<int>(gridDim.x) / ntiles;
+    const int L = static_cast<int>(blockIdx.x);
+    const int head = (BH - T) * ntiles;
+    if (L < head) {
+        bh = L / ntiles;
+        tile = L % ntiles;
+    } else {
+        const int r = L - head;
+        tile = r / T;
+        bh = BH - T + r % T;
+    }
+}
 VATTN_DEV uint32_t lane_id() { return threadIdx.x & 31; }
 
 // Per-warpgroup register budget hand-off (all 4 warps of the warpgroup execute it).
