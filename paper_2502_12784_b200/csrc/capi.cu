@@ -390,8 +390,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const cudaError_t ae = set_smem_once<mha_bwd_dq_gemm_kernel<kD, kBF16>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 2);
-        launch_pdl(kern, tile_grid(L.n_q, BH, bh_group(BH, 1ll * N * kD * 2, false)), dim3(256), smem, stream, mds, mk, mdq,
-                   p);  // K (each dS^T row is read once)
+        launch_pdl(kern, dim3(L.n_q * BH), dim3(256), smem, stream, mds, mk, mdq, p);
     } else {
         auto kern = mha_bwd_dq_kernel<kD, kBF16, kDrop>;
         constexpr int smem = DqCfg<kD>::kSmemBytes;

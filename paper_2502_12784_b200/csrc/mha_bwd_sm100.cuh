@@ -848,8 +848,9 @@ __global__ void __launch_bounds__(256, 1)
     const int warp = warp_id();
     const int lane = lane_id();
     const int nqb = p.n_q;
-    const int bh = grid_bh(nqb);
-    const int i = p.causal ? (nqb - 1 - grid_tile(nqb)) : grid_tile(nqb);
+    int bh, tile;
+    grid_item_tail(nqb, p.tail_units, bh, tile);  // same dispatch as the dK/dV grid
+    const int i = p.causal ? (nqb - 1 - tile) : tile;
     const int nk = p.causal ? i + 1 : p.n_q;
     if (threadIdx.x == 0) {
         if ((smem_u32(smem) & 1023u) != 0) __trap();
