@@ -556,6 +556,17 @@ VATTN_DEV float ex2_poly(float x) {
 #ifndef VATTN_POLY_DQ64
 #define VATTN_POLY_DQ64 0
 #endif
+// d = 128 dK/dV P pass: element pairs out of every 4 on the polynomial, per warpgroup.
+// Asymmetric by design: both warpgroups exponentiate at the same time, so moving half of
+// ONE warpgroup's work to the FMA pipe lets the two finish together (trace: -7 % per
+// step for the heaviest CTA; measured C3 / C5 backward -2.2 %).  Moving both
+// warpgroups' work (0/0 -> 4/4) is 10 % slower.
+#ifndef VATTN_POLY_DKDV_WG0
+#define VATTN_POLY_DKDV_WG0 0
+#endif
+#ifndef VATTN_POLY_DKDV_WG1
+#define VATTN_POLY_DKDV_WG1 2
+#endif
 template <int kD> struct PolyPeriod {
     static constexpr int fwd = kD == 64 ? VATTN_POLY_FWD64 : VATTN_POLY_FWD;
     static constexpr int dkdv = kD == 64 ? VATTN_POLY_DKDV64 : VATTN_POLY_DKDV;
