@@ -11,7 +11,8 @@ SHAPES = [(4, 16, 8192, 128, True), (4, 16, 8192, 128, False), (4, 16, 4096, 128
 if len(sys.argv) > 1:
     SHAPES = [tuple(json.loads(s)) for s in sys.argv[1:]]
 for B, H, N, d, causal in SHAPES:
-    q, k, v = (torch.randn((B, H, N, d), device="cuda").to(torch.bfloat16) for _ in range(3))
+    DT = torch.float16 if os.environ.get("DT") == "fp16" else torch.bfloat16
+    q, k, v = (torch.randn((B, H, N, d), device="cuda").to(DT) for _ in range(3))
     o = torch.empty_like(q); lse = torch.empty((B, H, N), device="cuda")
     f = lambda: vb.mha_forward(q, k, v, causal, out=o, lse=lse)
     for _ in range(3): f()

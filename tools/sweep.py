@@ -22,6 +22,7 @@ import ctypes as C
 import json
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -178,6 +179,7 @@ def main():
     burst, sust, src = measured_peaks()
     rows = []
     for cfg in CONFIGS:
+        time.sleep(2)  # let clocks / power recover so the row does not inherit the previous row's state
         r = run_one(*cfg, steps=args.steps if cfg[0] != "C5 (1 GPU)" else max(2, args.steps // 4))
         rows.append(r)
         print(json.dumps(r), flush=True)
@@ -196,7 +198,7 @@ def main():
                    "rows": rows, "traditional_vs_fused": trad}, f, indent=1)
     with open(os.path.join(args.out, f"{args.tag}_sweep.md"), "w") as f:
         f.write(f"# {args.tag} throughput sweep over BASELINE.json configs ({name}, 1 GPU)\n\n")
-        f.write("`python tools/sweep.py` -- CUDA events, 3 warm-up steps; TFLOPS = algorithmic "
+        f.write("`python tools/sweep.py` -- CUDA events, 3 warm-up steps, 2 s idle before each config; TFLOPS = algorithmic "
                 "14 B H N^2 d c / step time; % of the measured sustained bf16 peak "
                 f"({sust} TF/s, MEASURED_PEAKS.json).\n\n")
         f.write("| config | shape (B,H,N,d) | causal | dtype | step ms | TFLOPS | % peak | fwd TFLOPS | bwd TFLOPS |\n")
