@@ -49,3 +49,30 @@ def test_full_size_determinism_and_sampled_parity(name, shape, causal, dtype, sa
         check_lse(lse[sl].cpu().double().numpy(), rlse.double().cpu().numpy(), max_rel=2e-5)
         del ro, rlse, rdq, rdk, rdv
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("shape,causal", [((4, 16, 8192, 128), True), ((2, 15, 8192, 128), True),
+                                          ((1, 37, 4096, 128), True), ((2, 8, 4096, 64), False)],
+                         ids=["C3", "BH30-G15", "BH37-prime", "d64-noncausal"])
+def test_every_unit_equals_its_one_unit_slab(shape, causal):
+    """Dispatch order (grouped longest-first forward, longest-first tail of the dK/dV and
+    dQ grids) must not change which (b, h) unit a CTA computes: every unit of the full
+    problem is bitwise equal to the same unit computed alone as a one-unit slab, where
+    the mapping is trivial."""
+    B, H, N, d = shape
+    dtype = torch.bfloat16
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    q, k, v, do = (torch.randn(shape, generator=g, device="cuda").to(dtype) for _ in range(4))
+    o, lse = vb.mha_forward(q, k, v, causal)
+    dq, dk, dv = vb.mha_backward(q, k, v, o, do, lse, causal)
+    flat = [t.reshape(B * H, 1, N, -1) for t in (q, k, v, do, o, dq, dk, dv)]
+    lse_f = lse.reshape(B * H, 1, N)
+    for u in range(B * H):
+        qs, ks, vs, dos = (x[u:u + 1].contiguous() for x in flat[:4])
+        sl = (B, H, u, 1)
+        o1, l1 = vb.mha_forward(qs, ks, vs, causal, bh_slab=sl)
+        g1 = vb.mha_backward(qs, ks, vs, o1, dos, l1, causal, bh_slab=sl)
+        assert torch.equal(o1, flat[4][u:u + 1]) and torch.equal(l1, lse_f[u:u + 1]), u
+        for name, a, r in zip(("dq", "dk", "dv"), g1, flat[5:]):
+            assert torch.equal(a, r[u:u + 1]), (name, u)
