@@ -104,15 +104,17 @@ struct Job {
 
 int units_of(const vattn_config* c) { return c->bh_count ? c->bh_count : c->batch * c->heads; }
 
-// Slab size: every launch should still fill the GPU (>= 2 CTAs per SM over the
-// 128-row tiles of a head) while keeping enough slabs for the copies to overlap.
+// Slab size: every launch should still fill the GPU (one CTA per SM over the 128-row
+// tiles of a head) while keeping >= 16 slabs for the copies to overlap.  Measured at
+// C3 (64 units): 4 units per slab 12.05 ms per step, 5 units 13.6 ms, 2 units 12.4 ms,
+// 1 unit 16.4 ms; a fourth staging slot changes nothing.
 int slab_units(const vattn_config* c, int U) {
     static const int env = [] {  // tuning override: slabs per call
         const char* e = getenv("VATTN_HOST_SLABS");
         return e ? atoi(e) : 0;
     }();
     const int tiles = (c->seq_len + 127) / 128;
-    const int fill = (2 * 148 + tiles - 1) / tiles;
+    const int fill = (148 + tiles - 1) / tiles;
     const int for_overlap = (U + 15) / 16;  // aim for >= 16 slabs
     if (env > 0) return std::max(1, (U + env - 1) / env);
     return std::max(1, std::min(U, std::max(fill, for_overlap)));
