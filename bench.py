@@ -280,7 +280,7 @@ def main():
 
     def e2e_step():
         vb.mha_step_host(hq, hk, hv, hdo, causal, dropout_p=args.dropout, seed=1234,
-                         out=(ho, hlse, hdq, hdk, hdv))
+                         out=(ho, hlse, hdq, hdk, hdv), bh_slab=slab)
 
     e2e_ms = e2e_val = None
     if args.e2e_steps > 0:

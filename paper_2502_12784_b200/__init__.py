@@ -247,14 +247,14 @@ def _host_empty(shape, dtype, like):
 
 
 def mha_forward_host(q, k, v, causal: bool = False, softmax_scale: float = 0.0, dropout_p: float = 0.0,
-                     seed: int = 0, out=None, lse=None):
+                     seed: int = 0, out=None, lse=None, bh_slab=None):
     """C ABI ``mha_forward_host``: host tensors in and out, PCIe copies pipelined
     against the kernels slab by slab.  Pinned inputs give full overlap."""
     _check_host((q, k, v), q.shape, q.dtype, ("q", "k", "v"))
     B, H, N, d = q.shape
     out = _host_empty(q.shape, q.dtype, q) if out is None else out
     lse = _host_empty((B, H, N), torch.float32, q) if lse is None else lse
-    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
     rc = lib.mha_forward_host(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                               lse.data_ptr(), _stream())
     if rc:
@@ -263,13 +263,13 @@ def mha_forward_host(q, k, v, causal: bool = False, softmax_scale: float = 0.0, 
 
 
 def mha_backward_host(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: float = 0.0,
-                      dropout_p: float = 0.0, seed: int = 0, dq=None, dk=None, dv=None):
+                      dropout_p: float = 0.0, seed: int = 0, dq=None, dk=None, dv=None, bh_slab=None):
     """C ABI ``mha_backward_host`` on host tensors.  Returns (dq, dk, dv)."""
     _check_host((q, k, v, o, dout), q.shape, q.dtype, ("q", "k", "v", "o", "dout"))
     B, H, N, d = q.shape
     _check_host((lse,), (B, H, N), torch.float32, ("lse",))
     dq, dk, dv = (_host_empty(q.shape, q.dtype, q) if t is None else t for t in (dq, dk, dv))
-    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
     rc = lib.mha_backward_host(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
                                _stream())
@@ -279,7 +279,7 @@ def mha_backward_host(q, k, v, o, dout, lse, causal: bool = False, softmax_scale
 
 
 def mha_step_host(q, k, v, dout, causal: bool = False, softmax_scale: float = 0.0, dropout_p: float = 0.0,
-                  seed: int = 0, out=None):
+                  seed: int = 0, out=None, bh_slab=None):
     """C ABI ``mha_step_host``: forward + backward on host tensors with Q, K, V, dO
     crossing PCIe once.  ``out`` = optional preallocated (o, lse, dq, dk, dv).
     Returns (o, lse, dq, dk, dv)."""
@@ -289,7 +289,7 @@ def mha_step_host(q, k, v, dout, causal: bool = False, softmax_scale: float = 0.
         out = (_host_empty(q.shape, q.dtype, q), _host_empty((B, H, N), torch.float32, q),
                *(_host_empty(q.shape, q.dtype, q) for _ in range(3)))
     o, lse, dq, dk, dv = out
-    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed)
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
     rc = lib.mha_step_host(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), o.data_ptr(),
                            lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), _stream())
     if rc:

@@ -80,3 +80,24 @@ def test_host_errors():
     with pytest.raises(NotImplementedError):
         big = torch.zeros(1, 1, 64, 96, dtype=torch.float16)
         vb.mha_forward_host(big, big, big)
+
+
+def test_host_slab_calls_bitwise_with_dropout():
+    """Host-buffer entry points on a (b, h) slab (what a rank of a sharded run passes):
+    dropout masks follow the global (b, h), so each slab equals its rows of the
+    whole-problem device result."""
+    B, H, N, d, causal, dtype, p = 2, 3, 320, 128, True, torch.bfloat16, 0.15
+    q, k, v, do = workload(9, (B, H, N, d), dtype)
+    ref = _device_ref(q, k, v, do, causal, p)
+    flat = [t.reshape(B * H, 1, N, -1).cpu() for t in (q, k, v, do)]
+    for lo, hi in ((0, 4), (4, 6)):
+        sl = (B, H, lo, hi - lo)
+        hq, hk, hv, hdo = (x[lo:hi].contiguous().pin_memory() for x in flat)
+        got = vb.mha_step_host(hq, hk, hv, hdo, causal, dropout_p=p, seed=77, bh_slab=sl)
+        o, lse = vb.mha_forward_host(hq, hk, hv, causal, dropout_p=p, seed=77, bh_slab=sl)
+        g = vb.mha_backward_host(hq, hk, hv, o, hdo, lse, causal, dropout_p=p, seed=77, bh_slab=sl)
+        for name, a, r in zip(("o", "lse", "dq", "dk", "dv"), got, ref):
+            rf = r.reshape(B * H, *r.shape[2:])[lo:hi].cpu()
+            assert torch.equal(a.reshape(rf.shape), rf), (name, lo, hi)
+        for name, a, b in zip(("o", "lse", "dq", "dk", "dv"), (o, lse, *g), got):
+            assert torch.equal(a, b), ("separate calls", name, lo, hi)
