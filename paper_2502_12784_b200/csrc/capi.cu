@@ -218,9 +218,12 @@ int dkdv_tail_units(int BH, int n_q) {
         const char* e = getenv("VATTN_DKDV_TAIL_WAVES");
         return e ? atof(e) : 3.5;
     }();
-    int sms = 148;
+    static int sm_count[64] = {};  // per device, queried once
     int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    if (!sm_count[dev] && cudaDeviceGetAttribute(&sm_count[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        sm_count[dev] = 148;
+    const int sms = sm_count[dev];
     const int T = static_cast<int>((waves * sms + n_q - 1) / n_q);
     return T < 0 ? 0 : (T > BH ? BH : T);
 }
