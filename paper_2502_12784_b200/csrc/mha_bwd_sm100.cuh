@@ -364,38 +364,30 @@ __global__ void __launch_bounds__(384, 1)
                 for (int x = 0; x < 64; ++x)
                     keepm |= static_cast<uint64_t>(drop_keep(sDrop[64 * h + x], key, p.drop_thresh)) << x;
             }
-            // P = exp2(S c - lse2).  At d = 128 the two warpgroups exponentiate at the
-            // same time on the same MUFU; PolyPairs<kD, h> of every 4 element pairs go to
-            // the FMA-pipe polynomial instead (per warpgroup, so the split can be
-            // asymmetric).  At d = 64 the historical PolyPeriod mix is kept.
+            // P = exp2(S c - lse2).  The two warpgroups exponentiate at the same time on
+            // the same MUFU, so VATTN_POLY_DKDV*_WG1 of every 4 element pairs of warpgroup 1
+            // go to the FMA-pipe polynomial instead (asymmetric on purpose, sm100_ptx.cuh).
             auto p_pass = [&](auto npoly) {
                 constexpr int kNP = decltype(npoly)::value;
 #pragma unroll
                 for (int x = 0; x < 64; x += 4) {
                     const float4 l4 = *reinterpret_cast<const float4*>(lse2 + x);
-                    if constexpr (kD == 64) {
-                        pr[x + 0] = ex2_mix<PolyPeriod<kD>::dkdv>(x / 2, fmaf(pr[x + 0], sc, -l4.x));
-                        pr[x + 1] = ex2_mix<PolyPeriod<kD>::dkdv>(x / 2, fmaf(pr[x + 1], sc, -l4.y));
-                        pr[x + 2] = ex2(fmaf(pr[x + 2], sc, -l4.z));
-                        pr[x + 3] = ex2(fmaf(pr[x + 3], sc, -l4.w));
-                    } else {
-                        const float2 sc2 = make_float2(sc, sc);
-                        float2 a = ffma2(make_float2(pr[x], pr[x + 1]), sc2, make_float2(-l4.x, -l4.y));
-                        float2 b = ffma2(make_float2(pr[x + 2], pr[x + 3]), sc2, make_float2(-l4.z, -l4.w));
-                        const int pa = (x / 2) & 3, pb = (x / 2 + 1) & 3;  // pair slot within 4
-                        a = pa < kNP ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
-                        b = pb < kNP ? ex2_poly2(b) : make_float2(ex2(b.x), ex2(b.y));
-                        pr[x + 0] = a.x;
-                        pr[x + 1] = a.y;
-                        pr[x + 2] = b.x;
-                        pr[x + 3] = b.y;
-                    }
+                    const float2 sc2 = make_float2(sc, sc);
+                    float2 a = ffma2(make_float2(pr[x], pr[x + 1]), sc2, make_float2(-l4.x, -l4.y));
+                    float2 b = ffma2(make_float2(pr[x + 2], pr[x + 3]), sc2, make_float2(-l4.z, -l4.w));
+                    const int pa = (x / 2) & 3, pb = (x / 2 + 1) & 3;  // pair slot within 4
+                    a = pa < kNP ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
+                    b = pb < kNP ? ex2_poly2(b) : make_float2(ex2(b.x), ex2(b.y));
+                    pr[x + 0] = a.x;
+                    pr[x + 1] = a.y;
+                    pr[x + 2] = b.x;
+                    pr[x + 3] = b.y;
                 }
             };
             if (h == 0)  // warp-uniform
-                p_pass(std::integral_constant<int, VATTN_POLY_DKDV_WG0>{});
+                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DKDV64_WG0 : VATTN_POLY_DKDV_WG0>{});
             else
-                p_pass(std::integral_constant<int, VATTN_POLY_DKDV_WG1>{});
+                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DKDV64_WG1 : VATTN_POLY_DKDV_WG1>{});
             // masks only on the (warp-uniform) diagonal tile / the last key tile
             if ((p.causal && i == kb) || kb * 128 + 128 > N) {
                 // P = 0 for columns x < lim: key > query on the diagonal, all for keys >= N

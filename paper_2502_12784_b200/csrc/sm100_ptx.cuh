@@ -539,9 +539,6 @@ VATTN_DEV float ex2_poly(float x) {
 #ifndef VATTN_POLY_FWD
 #define VATTN_POLY_FWD 4
 #endif
-#ifndef VATTN_POLY_DKDV
-#define VATTN_POLY_DKDV 0
-#endif
 #ifndef VATTN_POLY_DQ
 #define VATTN_POLY_DQ 0
 #endif
@@ -550,26 +547,28 @@ VATTN_DEV float ex2_poly(float x) {
 #ifndef VATTN_POLY_FWD64
 #define VATTN_POLY_FWD64 4
 #endif
-#ifndef VATTN_POLY_DKDV64
-#define VATTN_POLY_DKDV64 4
-#endif
 #ifndef VATTN_POLY_DQ64
 #define VATTN_POLY_DQ64 0
 #endif
-// d = 128 dK/dV P pass: element pairs out of every 4 on the polynomial, per warpgroup.
-// Asymmetric by design: both warpgroups exponentiate at the same time, so moving half of
-// ONE warpgroup's work to the FMA pipe lets the two finish together (trace: -7 % per
-// step for the heaviest CTA; measured C3 / C5 backward -2.2 %).  Moving both
-// warpgroups' work (0/0 -> 4/4) is 10 % slower.
+// dK/dV P pass: element pairs out of every 4 on the polynomial, per warpgroup (d = 128
+// and d = 64 knobs).  Asymmetric by design: both warpgroups exponentiate at the same
+// time, so moving half of ONE warpgroup's work to the FMA pipe lets the two finish
+// together (trace: -7 % per step for the heaviest C3 CTA; measured backward -2.2 % at
+// C3 / C5, -5 % at C2 N = 4k and C4).  Moving both warpgroups' work is 10 % slower.
 #ifndef VATTN_POLY_DKDV_WG0
 #define VATTN_POLY_DKDV_WG0 0
 #endif
 #ifndef VATTN_POLY_DKDV_WG1
 #define VATTN_POLY_DKDV_WG1 2
 #endif
+#ifndef VATTN_POLY_DKDV64_WG0
+#define VATTN_POLY_DKDV64_WG0 0
+#endif
+#ifndef VATTN_POLY_DKDV64_WG1
+#define VATTN_POLY_DKDV64_WG1 2
+#endif
 template <int kD> struct PolyPeriod {
     static constexpr int fwd = kD == 64 ? VATTN_POLY_FWD64 : VATTN_POLY_FWD;
-    static constexpr int dkdv = kD == 64 ? VATTN_POLY_DKDV64 : VATTN_POLY_DKDV;
     static constexpr int dq = kD == 64 ? VATTN_POLY_DQ64 : VATTN_POLY_DQ;
 };
 // `pair` is an unrolled loop index, so the branch folds away at compile time.
