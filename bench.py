@@ -311,7 +311,8 @@ def main():
         base_ws = 2 * ((B * H * n_q * 128 * 4 + 255) // 256 * 256)
         tiles = B * H * (n_q * (n_q + 1) // 2 if causal else n_q * n_q)
         ds_bytes = tiles * 32768
-        dq_mode = "dS-GEMM" if ws.numel() > base_ws + 256 else "recompute"
+        # (dropout always takes the recompute path: its dS^T staging box is the row-hash buffer)
+        dq_mode = "dS-GEMM" if ws.numel() > base_ws + 256 and args.dropout == 0.0 else "recompute"
         achieved = f_dkdv / (dkdv_ms * 1e-3) / 1e12
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")

@@ -749,8 +749,24 @@ __global__ void __launch_bounds__(384, 1)
             const int kbase = j * 128 + 64 * h;
             if (p.causal && j == i) lim = min(lim, q - kbase);
             lim = min(lim, N - 1 - kbase);
+            // P = exp2(S c - lse2): packed scale-subtract; VATTN_POLY_DQ*_WG1 of every 4
+            // element pairs of warpgroup 1 on the FMA-pipe polynomial (asymmetric, as in
+            // the dK/dV kernel: the two warpgroups exponentiate at the same time)
+            auto p_pass = [&](auto npoly) {
+                constexpr int kNP = decltype(npoly)::value;
+                const float2 sc2 = make_float2(sc, sc), nl2 = make_float2(-lse2, -lse2);
 #pragma unroll
-            for (int x = 0; x < 64; ++x) pr[x] = ex2_mix<PolyPeriod<kD>::dq>(x / 2, fmaf(pr[x], sc, -lse2));
+                for (int x = 0; x < 64; x += 2) {
+                    float2 a = ffma2(make_float2(pr[x], pr[x + 1]), sc2, nl2);
+                    a = ((x / 2) & 3) < kNP ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
+                    pr[x] = a.x;
+                    pr[x + 1] = a.y;
+                }
+            };
+            if (h == 0)  // warp-uniform
+                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DQ64_WG0 : VATTN_POLY_DQ_WG0>{});
+            else
+                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DQ64_WG1 : VATTN_POLY_DQ_WG1>{});
             // masks only on the (warp-uniform) causal diagonal tile / the tile holding key N-1
             if ((p.causal && j == i) || kbase + 64 > N) {
 #pragma unroll

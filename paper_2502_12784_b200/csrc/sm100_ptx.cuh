@@ -567,6 +567,19 @@ VATTN_DEV float ex2_poly(float x) {
 #ifndef VATTN_POLY_DKDV64_WG1
 #define VATTN_POLY_DKDV64_WG1 2
 #endif
+// dQ recompute kernel P pass, same scheme (pairs out of every 4, per warpgroup)
+#ifndef VATTN_POLY_DQ_WG0
+#define VATTN_POLY_DQ_WG0 0
+#endif
+#ifndef VATTN_POLY_DQ_WG1
+#define VATTN_POLY_DQ_WG1 0
+#endif
+#ifndef VATTN_POLY_DQ64_WG0
+#define VATTN_POLY_DQ64_WG0 0
+#endif
+#ifndef VATTN_POLY_DQ64_WG1
+#define VATTN_POLY_DQ64_WG1 2
+#endif
 template <int kD> struct PolyPeriod {
     static constexpr int fwd = kD == 64 ? VATTN_POLY_FWD64 : VATTN_POLY_FWD;
     static constexpr int dq = kD == 64 ? VATTN_POLY_DQ64 : VATTN_POLY_DQ;
