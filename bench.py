@@ -215,7 +215,7 @@ def main():
     o = torch.empty_like(q)
     lse = torch.empty((B, H, N), device=dev, dtype=torch.float32)
     dq, dk, dv = (torch.empty_like(q) for _ in range(3))
-    ws = torch.empty(vb.workspace_bytes(B, H, N, d, causal, dtype), dtype=torch.uint8, device=dev)
+    ws = torch.empty(vb.workspace_bytes(B, H, N, d, causal, dtype, args.dropout), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
     # this rank's (b, h) slab of the global [B*world, H] problem (dropout masks use global (b, h))
@@ -311,8 +311,8 @@ def main():
         base_ws = 2 * ((B * H * n_q * 128 * 4 + 255) // 256 * 256)
         tiles = B * H * (n_q * (n_q + 1) // 2 if causal else n_q * n_q)
         ds_bytes = tiles * 32768
-        # (dropout always takes the recompute path: its dS^T staging box is the row-hash buffer)
-        dq_mode = "dS-GEMM" if ws.numel() > base_ws + 256 and args.dropout == 0.0 else "recompute"
+        # (with dropout the workspace also holds two keep-bit masks of BH * Npad^2 / 8 bytes)
+        dq_mode = "dS-GEMM" if ws.numel() > base_ws + 256 + (2 * B * H * n_q * 128 * n_q * 16 if args.dropout else 0) else "recompute"
         achieved = f_dkdv / (dkdv_ms * 1e-3) / 1e12
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")

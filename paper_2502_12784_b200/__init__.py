@@ -199,8 +199,10 @@ def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=N
     return out, lse
 
 
-def workspace_bytes(B, H, N, d, causal=False, dtype=torch.float16) -> int:
-    cfg = _Cfg(B, H, N, d, 1 if causal else 0, 0.0, VATTN_BF16 if dtype == torch.bfloat16 else VATTN_F16, 0.0, 0, 0, 0)
+def workspace_bytes(B, H, N, d, causal=False, dtype=torch.float16, dropout_p: float = 0.0) -> int:
+    """mha_backward workspace (dropout adds the keep-bit masks)."""
+    cfg = _Cfg(B, H, N, d, 1 if causal else 0, 0.0, VATTN_BF16 if dtype == torch.bfloat16 else VATTN_F16,
+               float(dropout_p), 0, 0, 0)
     return int(lib.mha_backward_workspace_bytes(C.byref(cfg)))
 
 

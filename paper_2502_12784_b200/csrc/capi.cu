@@ -286,7 +286,8 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
 }
 
 struct BwdLayout {
-    size_t lse2, dsum, ds, total;
+    size_t lse2, dsum, ds, mask, total;
+    bool drop_mask;          // dropout keep bits hashed once into the workspace
     int n_q, Npad;
     bool materialize_ds;     // dQ as a GEMM over materialised dS (else recompute S, dP)
     long long ds_tiles_per_bh;
@@ -318,10 +319,22 @@ BwdLayout bwd_layout(const vattn_config* c) {
     // (the dK/dV kernel's dS^T staging overlaps its dropout row-hash buffer)
     // d = 64 keeps the recompute path: its shorter dK/dV iterations pay more for the
     // staging than the dQ GEMM saves (measured: C2 -3 %, C3 at d = 128 +8 %).
-    L.materialize_ds = c->dropout_p > 0.0f
+    // Dropout: the keep bits are hashed once into two bit masks (query-major for the dQ
+    // kernel, key-major for the dK/dV kernel; BH * Npad^2 / 8 bytes each) instead of
+    // inside both kernels.  That also frees the dK/dV kernel's row-hash buffer for the
+    // dS^T staging box, so dropout can take the dQ GEMM path.  VATTN_DROP_MASK=0: hash
+    // in place (and recompute dQ).
+    static const bool mask_env = [] {
+        const char* e = getenv("VATTN_DROP_MASK");
+        return !(e && atoi(e) == 0);
+    }();
+    const size_t mask_bytes = BH * static_cast<size_t>(L.Npad) * (L.Npad / 8);
+    L.drop_mask = c->dropout_p > 0.0f && mask_env;
+    L.materialize_ds = c->dropout_p > 0.0f && !L.drop_mask
                            ? false
                            : (mode_env >= 0 ? mode_env == 1 : (c->head_dim == 128 && ds_bytes <= kDsCapBytes));
-    L.total = L.ds + (L.materialize_ds ? align256(ds_bytes) : 0);
+    L.mask = L.ds + (L.materialize_ds ? align256(ds_bytes) : 0);
+    L.total = L.mask + (L.drop_mask ? 2 * align256(mask_bytes) : 0);
     return L;
 }
 
@@ -375,6 +388,15 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     p.ds_out = L.materialize_ds ? reinterpret_cast<uint16_t*>(w + L.ds) : nullptr;
     p.ds_tiles_per_bh = L.ds_tiles_per_bh;
     p.tail_units = c->causal ? dkdv_tail_units(BH, L.n_q) : 0;
+    p.drop_mask = p.drop_maskT = nullptr;
+    if (L.drop_mask) {
+        uint32_t* m = reinterpret_cast<uint32_t*>(w + L.mask);
+        uint32_t* mt = reinterpret_cast<uint32_t*>(w + L.mask + align256(static_cast<size_t>(BH) * L.Npad * (L.Npad / 8)));
+        p.drop_mask = m;
+        p.drop_maskT = mt;
+        launch_pdl(mha_bwd_dropmask_kernel, dim3(148 * 8), dim3(256), 0, stream, m, mt, L.Npad, BH, p.H, p.bh_off,
+                   p.drop_seed, p.drop_thresh, c->causal);
+    }
     CUtensorMap mds;
     if (L.materialize_ds && !make_ds_map(&mds, p.ds_out, static_cast<long long>(BH) * L.ds_tiles_per_bh, kBF16))
         return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled (dS) failed");
@@ -409,7 +431,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     if (e == cudaSuccess) e = g_launch_err;
     g_launch_err = cudaSuccess;
     if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("mha_bwd launch: ") + cudaGetErrorString(e));
-    g_launches = 3;
+    g_launches = L.drop_mask ? 4 : 3;
     return VATTN_OK;
 }
 

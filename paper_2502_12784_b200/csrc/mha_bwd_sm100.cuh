@@ -102,7 +102,51 @@ struct BwdParams {
     uint16_t* ds_out;
     long long ds_tiles_per_bh;  // n_q^2, or n_q (n_q + 1) / 2 causal (lower triangle)
     int tail_units;             // dK/dV grid: last units dispatched longest-first (grid_item_tail)
+    // Dropout keep bits written once by mha_bwd_dropmask_kernel (nullptr = hash in place):
+    // drop_mask [unit][query][Npad/32 words] (bit = key), drop_maskT [unit][key][Npad/32]
+    // (bit = query).
+    const uint32_t* drop_mask;
+    const uint32_t* drop_maskT;
 };
+
+// Dropout keep bits of the backward, evaluated once (the reference's position hash,
+// rng.cpp:35-54) instead of in both backward kernels.  One warp per 32 x 32 (query,
+// key) block: lane l hashes query r0 + l against keys c0..c0+31 into one word of the
+// query-major mask; 32 ballots transpose the block into the key-major words the
+// key-major dK/dV kernel reads.  Causal: blocks wholly above the diagonal are skipped
+// (their positions are masked; the kernels never use those bits).
+__global__ void __launch_bounds__(256) mha_bwd_dropmask_kernel(uint32_t* __restrict__ mask,
+                                                               uint32_t* __restrict__ maskT, int Npad, int BH,
+                                                               int H, int bh_off, uint64_t seed, uint64_t thresh,
+                                                               int causal) {
+    const int W = Npad / 32;
+    const int lane = threadIdx.x & 31;
+    const long long nblk = static_cast<long long>(BH) * W * W;
+    const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    griddep_wait();
+    for (long long blk = gw; blk < nblk; blk += nw) {
+        const int bh = static_cast<int>(blk / (static_cast<long long>(W) * W));
+        const int rem = static_cast<int>(blk - static_cast<long long>(bh) * W * W);
+        const int rw = rem / W, cw = rem % W;  // query word (row block), key word (column block)
+        if (causal && cw > rw) continue;       // warp-uniform
+        const int r0 = rw * 32, c0 = cw * 32;
+        const DropRow dr = drop_row(drop_bh_base(seed, (bh + bh_off) / H, (bh + bh_off) % H), r0 + lane);
+        uint32_t w = 0;
+#pragma unroll 8
+        for (int b = 0; b < 32; ++b) w |= static_cast<uint32_t>(drop_keep(dr, c0 + b, thresh)) << b;
+        const size_t base = static_cast<size_t>(bh) * Npad;
+        mask[(base + r0 + lane) * W + cw] = w;
+        uint32_t t = 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t bt = __ballot_sync(0xffffffffu, (w >> b) & 1u);  // bit l = query r0 + l, key c0 + b
+            if (lane == b) t = bt;
+        }
+        maskT[(base + c0 + lane) * W + rw] = t;
+    }
+    griddep_launch_dependents();
+}
 
 // Index of dS^T tile (query tile i, key tile kb) within one (b, h).
 VATTN_DEV long long ds_tile_index(const BwdParams& p, int i, int kb) {
@@ -353,7 +397,10 @@ __global__ void __launch_bounds__(384, 1)
             tmem_wait_ld();
             const int qbase = i * 128 + 64 * h;
             uint64_t keepm = ~0ull;  // dropout keep bits of this thread's 64 (query, key) positions
-            if constexpr (kDrop) {
+            if (kDrop && p.drop_maskT) {  // 64 query bits of this key row: one 8-byte load
+                keepm = *reinterpret_cast<const unsigned long long*>(
+                    p.drop_maskT + (static_cast<size_t>(bh) * p.Npad + (kb * 128 + r)) * (p.Npad / 32) + qbase / 32);
+            } else if constexpr (kDrop) {
                 // row prefixes of the reference hash for this warpgroup's 64 queries
                 named_bar_sync(1 + h, 128);  // previous step's readers are done
                 if ((warp & 3) * 32 + lane < 64)
@@ -798,10 +845,17 @@ __global__ void __launch_bounds__(384, 1)
                     tmem_wait_ld();
                 }
                 if constexpr (kDrop) {  // dS = P o (drop o dP - D)
+                    if (p.drop_mask) {
+                        const uint32_t kw = p.drop_mask[(static_cast<size_t>(bh) * p.Npad + q) * (p.Npad / 32) +
+                                                        (j * 128 + 64 * h + 32 * c) / 32];
 #pragma unroll
-                    for (int x = 0; x < 32; ++x) {
-                        const int col = j * 128 + 64 * h + 32 * c + x;
-                        dpv[x] = drop_keep(drow, col, p.drop_thresh) ? dpv[x] * p.inv_keep : 0.0f;
+                        for (int x = 0; x < 32; ++x) dpv[x] = (kw >> x) & 1u ? dpv[x] * p.inv_keep : 0.0f;
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < 32; ++x) {
+                            const int col = j * 128 + 64 * h + 32 * c + x;
+                            dpv[x] = drop_keep(drow, col, p.drop_thresh) ? dpv[x] * p.inv_keep : 0.0f;
+                        }
                     }
                 }
                 const float2 nd2 = make_float2(-dsum, -dsum);
