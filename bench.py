@@ -221,10 +221,15 @@ def main():
     # this rank's (b, h) slab of the global [B*world, H] problem (dropout masks use global (b, h))
     slab = (B * world, H, rank * B * H, B * H) if world > 1 else None
 
+    # dropout: the forward keeps its keep bits for the backward (as the autograd binding does)
+    mask = (torch.empty(vb.dropout_mask_bytes(q, causal, args.dropout, slab), dtype=torch.uint8, device=dev)
+            if args.dropout > 0 else None)
+
     def step():
-        vb.mha_forward(q, k, v, causal, out=o, lse=lse, dropout_p=args.dropout, seed=1234, bh_slab=slab)
+        vb.mha_forward(q, k, v, causal, out=o, lse=lse, dropout_p=args.dropout, seed=1234, bh_slab=slab,
+                       drop_mask=mask)
         vb.mha_backward(q, k, v, o, do, lse, causal, dq=dq, dk=dk, dv=dv, workspace=ws,
-                        dropout_p=args.dropout, seed=1234, bh_slab=slab)
+                        dropout_p=args.dropout, seed=1234, bh_slab=slab, drop_mask=mask)
 
     for _ in range(args.warmup):
         step()

@@ -98,6 +98,23 @@ int mha_backward(const vattn_config* cfg, const void* q, const void* k, const vo
                  const void* o, const void* dout, const float* lse, void* dq, void* dk, void* dv,
                  void* workspace, size_t workspace_bytes, void* stream);
 
+/* Dropout keep bits kept from the forward for the backward (optional fast path).
+ * mha_dropout_mask_bytes(cfg): size of the mask, B*H*Npad*Npad/8 bytes with Npad = N
+ * rounded up to 128 (0 when dropout_p == 0 or cfg is invalid).
+ * mha_forward_dropout_mask: mha_forward that also stores the keep bits it computes
+ * (query-major, one bit per (query, key) position it visits) into `drop_mask`.
+ * mha_backward_dropout_mask: mha_backward that reads those bits instead of hashing
+ * the positions again (same results, bit for bit; `drop_mask` must come from
+ * mha_forward_dropout_mask with the same cfg).  Both require dropout_p > 0 and a
+ * 256-byte aligned mask.  Without them the backward hashes the keep bits itself. */
+size_t mha_dropout_mask_bytes(const vattn_config* cfg);
+int mha_forward_dropout_mask(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o,
+                             float* lse, void* drop_mask, void* stream);
+int mha_backward_dropout_mask(const vattn_config* cfg, const void* q, const void* k, const void* v,
+                              const void* o, const void* dout, const float* lse, const void* drop_mask,
+                              void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
 /* D = rowsum(dO o O) per query row ([B, H, N] binary32, products widened before the
  * sum) -- vattn::compute_dpsum (proj/include/vattn/backward.hpp:43,
  * attention_backward.cpp:44-57), the backward's preprocessing pass on its own. */

@@ -70,6 +70,12 @@ def _load():
     lib.mha_step_host.restype = C.c_int
     lib.vattn_dropout_digest.argtypes = [C.POINTER(_Cfg), C.c_int, C.c_int, vp, vp]
     lib.vattn_dropout_digest.restype = C.c_int
+    lib.mha_dropout_mask_bytes.argtypes = [C.POINTER(_Cfg)]
+    lib.mha_dropout_mask_bytes.restype = C.c_size_t
+    lib.mha_forward_dropout_mask.argtypes = [C.POINTER(_Cfg)] + [vp] * 7
+    lib.mha_forward_dropout_mask.restype = C.c_int
+    lib.mha_backward_dropout_mask.argtypes = [C.POINTER(_Cfg)] + [vp] * 11 + [C.c_size_t, vp]
+    lib.mha_backward_dropout_mask.restype = C.c_int
     lib.mha_dpsum.argtypes = [C.POINTER(_Cfg)] + [vp] * 4
     lib.mha_dpsum.restype = C.c_int
     lib.vattn_last_error.restype = C.c_char_p
@@ -183,7 +189,7 @@ def _pad(t: torch.Tensor, dn: int) -> torch.Tensor:
 
 
 def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=None, lse=None,
-                dropout_p: float = 0.0, seed: int = 0, bh_slab=None):
+                dropout_p: float = 0.0, seed: int = 0, bh_slab=None, drop_mask=None):
     """C ABI ``mha_forward`` on CUDA tensors [B, H, N, d] (d in {64, 128}).
     Returns (out, lse) with lse [B, H, N] fp32 natural-log.  ``dropout_p > 0``
     applies the reference's dropout (keep bits = vattn::dropout_keep(seed, b, h, row, col, p))."""
@@ -192,11 +198,27 @@ def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=N
     out = torch.empty_like(q) if out is None else out
     lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
     cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
-    rc = lib.mha_forward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                         lse.data_ptr(), _stream())
+    if drop_mask is not None:  # also keep the dropout keep bits for mha_backward(drop_mask=...)
+        _check_mask(drop_mask, cfg)
+        rc = lib.mha_forward_dropout_mask(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                          lse.data_ptr(), drop_mask.data_ptr(), _stream())
+    else:
+        rc = lib.mha_forward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                             lse.data_ptr(), _stream())
     if rc:
         _raise(rc, "mha_forward")
     return out, lse
+
+
+def dropout_mask_bytes(q, causal: bool = False, dropout_p: float = 0.0, bh_slab=None) -> int:
+    """Bytes of the keep-bit mask mha_forward(drop_mask=...) fills (0 without dropout)."""
+    return int(lib.mha_dropout_mask_bytes(C.byref(_cfg(q, causal, 0.0, dropout_p, 0, bh_slab))))
+
+
+def _check_mask(m, cfg):
+    need = int(lib.mha_dropout_mask_bytes(C.byref(cfg)))
+    if not m.is_cuda or m.numel() * m.element_size() < need or m.data_ptr() % 256:
+        raise ValueError(f"drop_mask must be a 256-byte aligned CUDA buffer of >= {need} bytes")
 
 
 def workspace_bytes(B, H, N, d, causal=False, dtype=torch.float16, dropout_p: float = 0.0) -> int:
@@ -207,7 +229,8 @@ def workspace_bytes(B, H, N, d, causal=False, dtype=torch.float16, dropout_p: fl
 
 
 def mha_backward(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: float = 0.0,
-                 dq=None, dk=None, dv=None, workspace=None, dropout_p: float = 0.0, seed: int = 0, bh_slab=None):
+                 dq=None, dk=None, dv=None, workspace=None, dropout_p: float = 0.0, seed: int = 0, bh_slab=None,
+                 drop_mask=None):
     """C ABI ``mha_backward`` on CUDA tensors.  Returns (dq, dk, dv).
     ``bh_slab=(B, H, offset, count)``: the tensors are units [offset, offset+count)
     of a global (B, H) problem (used by (b, h) sharding)."""
@@ -225,9 +248,16 @@ def mha_backward(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: flo
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(q) if dk is None else dk
     dv = torch.empty_like(q) if dv is None else dv
-    rc = lib.mha_backward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
-                          dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
-                          workspace.data_ptr(), workspace.numel(), _stream())
+    if drop_mask is not None:  # the forward's keep bits (mha_forward(drop_mask=...))
+        _check_mask(drop_mask, cfg)
+        rc = lib.mha_backward_dropout_mask(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                           dout.data_ptr(), lse.data_ptr(), drop_mask.data_ptr(), dq.data_ptr(),
+                                           dk.data_ptr(), dv.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                                           _stream())
+    else:
+        rc = lib.mha_backward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                              dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                              workspace.data_ptr(), workspace.numel(), _stream())
     if rc:
         _raise(rc, "mha_backward")
     return dq, dk, dv
@@ -370,8 +400,12 @@ class MHAFunction(torch.autograd.Function):
         dn = _native_dim(d)
         qp, kp, vp = (_pad(x.contiguous(), dn) for x in (q, k, v))
         scale = softmax_scale if softmax_scale > 0 else 1.0 / math.sqrt(d)
-        o, lse = mha_forward(qp, kp, vp, causal, scale, dropout_p=dropout_p, seed=seed)
+        mask = None
+        if dropout_p > 0.0:  # keep the forward's keep bits: the backward skips re-hashing them
+            mask = torch.empty(dropout_mask_bytes(qp, causal, dropout_p), dtype=torch.uint8, device=qp.device)
+        o, lse = mha_forward(qp, kp, vp, causal, scale, dropout_p=dropout_p, seed=seed, drop_mask=mask)
         ctx.save_for_backward(qp, kp, vp, o, lse)
+        ctx.drop_mask = mask
         ctx.causal, ctx.scale, ctx.d, ctx.dropout_p, ctx.seed = causal, scale, d, dropout_p, seed
         return o[..., :d] if dn != d else o
 
@@ -380,7 +414,7 @@ class MHAFunction(torch.autograd.Function):
         qp, kp, vp, o, lse = ctx.saved_tensors
         dop = _pad(do.contiguous(), qp.shape[-1])
         dq, dk, dv = mha_backward(qp, kp, vp, o, dop, lse, ctx.causal, ctx.scale,
-                                  dropout_p=ctx.dropout_p, seed=ctx.seed)
+                                  dropout_p=ctx.dropout_p, seed=ctx.seed, drop_mask=ctx.drop_mask)
         d = ctx.d
         return dq[..., :d], dk[..., :d], dv[..., :d], None, None, None, None
 

@@ -251,7 +251,7 @@ cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, int sme
 
 template <int kD, bool kBF16, bool kDrop>
 int launch_forward(const vattn_config* c, const void* q, const void* k, const void* v, void* o,
-                   float* lse, cudaStream_t stream) {
+                   float* lse, uint32_t* drop_mask, cudaStream_t stream) {
     const int BH = units(c), N = c->seq_len;
     CUtensorMap mq, mk, mv, mo;
     if (!make_map(&mq, q, BH, N, kD, kBF16) || !make_map(&mk, k, BH, N, kD, kBF16) ||
@@ -272,6 +272,8 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     p.causal = c->causal;
     p.scale_log2 = eff_scale(c) * kLog2e;
     set_dropout(c, &p.H, &p.bh_off, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
+    p.drop_mask = drop_mask;
+    p.mask_words = (N + 127) / 128 * 4;
     const dim3 grid = tile_grid((N + 255) / 256, BH, c->causal ? bh_group(BH, 2ll * N * kD * 2, true) : 1);  // K, V
     {
         ProfScope prof(stream, 0);
@@ -319,11 +321,11 @@ BwdLayout bwd_layout(const vattn_config* c) {
     // (the dK/dV kernel's dS^T staging overlaps its dropout row-hash buffer)
     // d = 64 keeps the recompute path: its shorter dK/dV iterations pay more for the
     // staging than the dQ GEMM saves (measured: C2 -3 %, C3 at d = 128 +8 %).
-    // Dropout: the keep bits are hashed once into two bit masks (query-major for the dQ
-    // kernel, key-major for the dK/dV kernel; BH * Npad^2 / 8 bytes each) instead of
-    // inside both kernels.  That also frees the dK/dV kernel's row-hash buffer for the
-    // dS^T staging box, so dropout can take the dQ GEMM path.  VATTN_DROP_MASK=0: hash
-    // in place (and recompute dQ).
+    // Dropout: both backward kernels read the keep bits from a query-major bit mask
+    // (BH * Npad^2 / 8 bytes) -- the forward's own (mha_forward_dropout_mask) or one
+    // hashed here once -- instead of hashing every position twice.  That also frees the
+    // dK/dV kernel's row-hash buffer for the dS^T staging box, so dropout takes the dQ
+    // GEMM path.  VATTN_DROP_MASK=0: hash in place (and recompute dQ).
     static const bool mask_env = [] {
         const char* e = getenv("VATTN_DROP_MASK");
         return !(e && atoi(e) == 0);
@@ -334,7 +336,7 @@ BwdLayout bwd_layout(const vattn_config* c) {
                            ? false
                            : (mode_env >= 0 ? mode_env == 1 : (c->head_dim == 128 && ds_bytes <= kDsCapBytes));
     L.mask = L.ds + (L.materialize_ds ? align256(ds_bytes) : 0);
-    L.total = L.mask + (L.drop_mask ? 2 * align256(mask_bytes) : 0);
+    L.total = L.mask + (L.drop_mask ? align256(mask_bytes) : 0);
     return L;
 }
 
@@ -351,7 +353,7 @@ cudaError_t set_smem_once(int bytes) {
 template <int kD, bool kBF16, bool kDrop>
 int launch_backward(const vattn_config* c, const void* q, const void* k, const void* v,
                     const void* o, const void* dout, const float* lse, void* dq, void* dk,
-                    void* dv, void* ws, cudaStream_t stream) {
+                    void* dv, void* ws, const uint32_t* ext_mask, cudaStream_t stream) {
     const int BH = units(c), N = c->seq_len;
     const BwdLayout L = bwd_layout(c);
     uint8_t* w = static_cast<uint8_t*>(ws);
@@ -388,14 +390,18 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     p.ds_out = L.materialize_ds ? reinterpret_cast<uint16_t*>(w + L.ds) : nullptr;
     p.ds_tiles_per_bh = L.ds_tiles_per_bh;
     p.tail_units = c->causal ? dkdv_tail_units(BH, L.n_q) : 0;
-    p.drop_mask = p.drop_maskT = nullptr;
+    p.drop_mask = nullptr;
+    bool mask_kernel = false;
     if (L.drop_mask) {
-        uint32_t* m = reinterpret_cast<uint32_t*>(w + L.mask);
-        uint32_t* mt = reinterpret_cast<uint32_t*>(w + L.mask + align256(static_cast<size_t>(BH) * L.Npad * (L.Npad / 8)));
-        p.drop_mask = m;
-        p.drop_maskT = mt;
-        launch_pdl(mha_bwd_dropmask_kernel, dim3(148 * 8), dim3(256), 0, stream, m, mt, L.Npad, BH, p.H, p.bh_off,
-                   p.drop_seed, p.drop_thresh, c->causal);
+        if (ext_mask) {  // the forward's own keep bits (mha_forward_dropout_mask)
+            p.drop_mask = ext_mask;
+        } else {
+            uint32_t* m = reinterpret_cast<uint32_t*>(w + L.mask);
+            p.drop_mask = m;
+            mask_kernel = true;
+            launch_pdl(mha_bwd_dropmask_kernel, dim3(148 * 8), dim3(256), 0, stream, m, L.Npad, BH, p.H, p.bh_off,
+                       p.drop_seed, p.drop_thresh, c->causal);
+        }
     }
     CUtensorMap mds;
     if (L.materialize_ds && !make_ds_map(&mds, p.ds_out, static_cast<long long>(BH) * L.ds_tiles_per_bh, kBF16))
@@ -431,7 +437,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     if (e == cudaSuccess) e = g_launch_err;
     g_launch_err = cudaSuccess;
     if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("mha_bwd launch: ") + cudaGetErrorString(e));
-    g_launches = L.drop_mask ? 4 : 3;
+    g_launches = mask_kernel ? 4 : 3;
     return VATTN_OK;
 }
 
@@ -500,8 +506,8 @@ int vattn_profile_read(int kind, double* ms_total, int* launches) {
     return VATTN_OK;
 }
 
-int mha_forward(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o,
-                float* lse, void* stream) {
+static int forward_impl(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o, float* lse,
+                        uint32_t* mask, void* stream) {
     g_launches = 0;
     int rc = validate(cfg);
     if (rc) return rc;
@@ -512,15 +518,37 @@ int mha_forward(const vattn_config* cfg, const void* q, const void* k, const voi
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int sel = (cfg->head_dim == 128 ? 4 : 0) | (cfg->dtype == VATTN_BF16 ? 2 : 0) | (cfg->dropout_p > 0.0f ? 1 : 0);
     switch (sel) {
-        case 0: return launch_forward<64, false, false>(cfg, q, k, v, o, lse, s);
-        case 1: return launch_forward<64, false, true>(cfg, q, k, v, o, lse, s);
-        case 2: return launch_forward<64, true, false>(cfg, q, k, v, o, lse, s);
-        case 3: return launch_forward<64, true, true>(cfg, q, k, v, o, lse, s);
-        case 4: return launch_forward<128, false, false>(cfg, q, k, v, o, lse, s);
-        case 5: return launch_forward<128, false, true>(cfg, q, k, v, o, lse, s);
-        case 6: return launch_forward<128, true, false>(cfg, q, k, v, o, lse, s);
-        default: return launch_forward<128, true, true>(cfg, q, k, v, o, lse, s);
+        case 0: return launch_forward<64, false, false>(cfg, q, k, v, o, lse, mask, s);
+        case 1: return launch_forward<64, false, true>(cfg, q, k, v, o, lse, mask, s);
+        case 2: return launch_forward<64, true, false>(cfg, q, k, v, o, lse, mask, s);
+        case 3: return launch_forward<64, true, true>(cfg, q, k, v, o, lse, mask, s);
+        case 4: return launch_forward<128, false, false>(cfg, q, k, v, o, lse, mask, s);
+        case 5: return launch_forward<128, false, true>(cfg, q, k, v, o, lse, mask, s);
+        case 6: return launch_forward<128, true, false>(cfg, q, k, v, o, lse, mask, s);
+        default: return launch_forward<128, true, true>(cfg, q, k, v, o, lse, mask, s);
     }
+}
+
+int mha_forward(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o,
+                float* lse, void* stream) {
+    return forward_impl(cfg, q, k, v, o, lse, nullptr, stream);
+}
+
+size_t mha_dropout_mask_bytes(const vattn_config* cfg) {
+    if (validate(cfg) || cfg->dropout_p <= 0.0f) return 0;
+    const size_t Npad = static_cast<size_t>((cfg->seq_len + 127) / 128) * 128;
+    return static_cast<size_t>(units(cfg)) * Npad * (Npad / 8);
+}
+
+int mha_forward_dropout_mask(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o, float* lse,
+                             void* drop_mask, void* stream) {
+    g_launches = 0;
+    int rc = validate(cfg);
+    if (rc) return rc;
+    if (cfg->dropout_p <= 0.0f) return fail(VATTN_EINVAL, "mha_forward_dropout_mask: dropout_p must be > 0");
+    if (!drop_mask || (reinterpret_cast<uintptr_t>(drop_mask) & 255u) != 0)
+        return fail(VATTN_EINVAL, "mha_forward_dropout_mask: mask must be non-null and 256-byte aligned");
+    return forward_impl(cfg, q, k, v, o, lse, static_cast<uint32_t*>(drop_mask), stream);
 }
 
 int mha_dpsum(const vattn_config* cfg, const void* o, const void* dout, float* d_rows, void* stream) {
@@ -590,9 +618,9 @@ size_t mha_backward_workspace_bytes(const vattn_config* cfg) {
     return bwd_layout(cfg).total;
 }
 
-int mha_backward(const vattn_config* cfg, const void* q, const void* k, const void* v,
-                 const void* o, const void* dout, const float* lse, void* dq, void* dk, void* dv,
-                 void* workspace, size_t workspace_bytes, void* stream) {
+static int backward_impl(const vattn_config* cfg, const void* q, const void* k, const void* v, const void* o,
+                         const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                         size_t workspace_bytes, const uint32_t* mask, void* stream) {
     g_launches = 0;
     int rc = validate(cfg);
     if (rc) return rc;
@@ -608,7 +636,7 @@ int mha_backward(const vattn_config* cfg, const void* q, const void* k, const vo
     if ((rc = check_device())) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int sel = (cfg->head_dim == 128 ? 4 : 0) | (cfg->dtype == VATTN_BF16 ? 2 : 0) | (cfg->dropout_p > 0.0f ? 1 : 0);
-#define VATTN_BWD(D, BF, DR) launch_backward<D, BF, DR>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, s)
+#define VATTN_BWD(D, BF, DR) launch_backward<D, BF, DR>(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, mask, s)
     switch (sel) {
         case 0: return VATTN_BWD(64, false, false);
         case 1: return VATTN_BWD(64, false, true);
@@ -620,6 +648,44 @@ int mha_backward(const vattn_config* cfg, const void* q, const void* k, const vo
         default: return VATTN_BWD(128, true, true);
     }
 #undef VATTN_BWD
+}
+
+int mha_backward(const vattn_config* cfg, const void* q, const void* k, const void* v,
+                 const void* o, const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                 void* workspace, size_t workspace_bytes, void* stream) {
+    return backward_impl(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, workspace_bytes, nullptr, stream);
+}
+
+// internal (capi_host.cu): forward + backward of one slab on device buffers.  With
+// dropout the forward keeps its keep bits in the workspace's mask region and the
+// backward reads them (no second hash pass).
+int vattn_step_device_(const vattn_config* cfg, const void* q, const void* k, const void* v, const void* dout, void* o,
+                       float* lse, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+    int rc = validate(cfg);
+    if (rc) return rc;
+    uint32_t* mask = nullptr;
+    if (cfg->dropout_p > 0.0f) {
+        const BwdLayout L = bwd_layout(cfg);
+        if (L.drop_mask && workspace && workspace_bytes >= L.total)
+            mask = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) + L.mask);
+    }
+    rc = forward_impl(cfg, q, k, v, o, lse, mask, stream);
+    if (rc) return rc;
+    return backward_impl(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, workspace_bytes, mask, stream);
+}
+
+int mha_backward_dropout_mask(const vattn_config* cfg, const void* q, const void* k, const void* v, const void* o,
+                              const void* dout, const float* lse, const void* drop_mask, void* dq, void* dk, void* dv,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    int rc = validate(cfg);
+    if (rc) return rc;
+    if (cfg->dropout_p <= 0.0f) return fail(VATTN_EINVAL, "mha_backward_dropout_mask: dropout_p must be > 0");
+    if (!drop_mask || (reinterpret_cast<uintptr_t>(drop_mask) & 255u) != 0)
+        return fail(VATTN_EINVAL, "mha_backward_dropout_mask: mask must be non-null and 256-byte aligned");
+    return backward_impl(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, workspace_bytes,
+                         static_cast<const uint32_t*>(drop_mask), stream);
 }
 
 }  // extern "C"

@@ -220,6 +220,9 @@ size_t lse_unit(const vattn_config* c) { return static_cast<size_t>(c->seq_len) 
 
 }  // namespace
 extern "C" int vattn_validate_(const vattn_config* cfg);  // capi.cu
+extern "C" int vattn_step_device_(const vattn_config* cfg, const void* q, const void* k, const void* v,
+                                  const void* dout, void* o, float* lse, void* dq, void* dk, void* dv,
+                                  void* workspace, size_t workspace_bytes, void* stream);  // capi.cu
 namespace {
 
 // The device entry points' own validation (same codes and messages).
@@ -239,10 +242,8 @@ int run_bwd(const vattn_config* s, void* const* in, void* const* out, void* ws, 
 }
 
 int run_step(const vattn_config* s, void* const* in, void* const* out, void* ws, size_t wsb, cudaStream_t st) {
-    const int rc = mha_forward(s, in[0], in[1], in[2], out[0], static_cast<float*>(out[1]), st);
-    if (rc) return rc;
-    return mha_backward(s, in[0], in[1], in[2], out[0], in[3], static_cast<const float*>(out[1]), out[2], out[3],
-                        out[4], ws, wsb, st);
+    return vattn_step_device_(s, in[0], in[1], in[2], in[3], out[0], static_cast<float*>(out[1]), out[2], out[3],
+                              out[4], ws, wsb, st);
 }
 
 template <typename F>

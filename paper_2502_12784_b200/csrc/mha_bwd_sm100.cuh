@@ -102,22 +102,18 @@ struct BwdParams {
     uint16_t* ds_out;
     long long ds_tiles_per_bh;  // n_q^2, or n_q (n_q + 1) / 2 causal (lower triangle)
     int tail_units;             // dK/dV grid: last units dispatched longest-first (grid_item_tail)
-    // Dropout keep bits written once by mha_bwd_dropmask_kernel (nullptr = hash in place):
-    // drop_mask [unit][query][Npad/32 words] (bit = key), drop_maskT [unit][key][Npad/32]
-    // (bit = query).
+    // Dropout keep bits [unit][query][Npad/32 words] (bit = key), written by the forward
+    // (mha_forward_dropout_mask) or by mha_bwd_dropmask_kernel; nullptr = hash in place.
     const uint32_t* drop_mask;
-    const uint32_t* drop_maskT;
 };
 
-// Dropout keep bits of the backward, evaluated once (the reference's position hash,
-// rng.cpp:35-54) instead of in both backward kernels.  One warp per 32 x 32 (query,
-// key) block: lane l hashes query r0 + l against keys c0..c0+31 into one word of the
-// query-major mask; 32 ballots transpose the block into the key-major words the
-// key-major dK/dV kernel reads.  Causal: blocks wholly above the diagonal are skipped
-// (their positions are masked; the kernels never use those bits).
-__global__ void __launch_bounds__(256) mha_bwd_dropmask_kernel(uint32_t* __restrict__ mask,
-                                                               uint32_t* __restrict__ maskT, int Npad, int BH,
-                                                               int H, int bh_off, uint64_t seed, uint64_t thresh,
+// Dropout keep bits of the backward when the forward did not keep them: the
+// reference's position hash (rng.cpp:35-54) evaluated once per position into the
+// query-major mask, instead of inside both backward kernels.  One warp per 32 x 32
+// (query, key) block, lane l = query r0 + l.  Causal: blocks wholly above the diagonal
+// are skipped (those positions are masked; the kernels never use their bits).
+__global__ void __launch_bounds__(256) mha_bwd_dropmask_kernel(uint32_t* __restrict__ mask, int Npad, int BH, int H,
+                                                               int bh_off, uint64_t seed, uint64_t thresh,
                                                                int causal) {
     const int W = Npad / 32;
     const int lane = threadIdx.x & 31;
@@ -130,20 +126,11 @@ __global__ void __launch_bounds__(256) mha_bwd_dropmask_kernel(uint32_t* __restr
         const int rem = static_cast<int>(blk - static_cast<long long>(bh) * W * W);
         const int rw = rem / W, cw = rem % W;  // query word (row block), key word (column block)
         if (causal && cw > rw) continue;       // warp-uniform
-        const int r0 = rw * 32, c0 = cw * 32;
-        const DropRow dr = drop_row(drop_bh_base(seed, (bh + bh_off) / H, (bh + bh_off) % H), r0 + lane);
+        const DropRow dr = drop_row(drop_bh_base(seed, (bh + bh_off) / H, (bh + bh_off) % H), rw * 32 + lane);
         uint32_t w = 0;
 #pragma unroll 8
-        for (int b = 0; b < 32; ++b) w |= static_cast<uint32_t>(drop_keep(dr, c0 + b, thresh)) << b;
-        const size_t base = static_cast<size_t>(bh) * Npad;
-        mask[(base + r0 + lane) * W + cw] = w;
-        uint32_t t = 0;
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            const uint32_t bt = __ballot_sync(0xffffffffu, (w >> b) & 1u);  // bit l = query r0 + l, key c0 + b
-            if (lane == b) t = bt;
-        }
-        maskT[(base + c0 + lane) * W + rw] = t;
+        for (int b = 0; b < 32; ++b) w |= static_cast<uint32_t>(drop_keep(dr, cw * 32 + b, thresh)) << b;
+        mask[(static_cast<size_t>(bh) * Npad + rw * 32 + lane) * W + cw] = w;
     }
     griddep_launch_dependents();
 }
@@ -397,9 +384,24 @@ __global__ void __launch_bounds__(384, 1)
             tmem_wait_ld();
             const int qbase = i * 128 + 64 * h;
             uint64_t keepm = ~0ull;  // dropout keep bits of this thread's 64 (query, key) positions
-            if (kDrop && p.drop_maskT) {  // 64 query bits of this key row: one 8-byte load
-                keepm = *reinterpret_cast<const unsigned long long*>(
-                    p.drop_maskT + (static_cast<size_t>(bh) * p.Npad + (kb * 128 + r)) * (p.Npad / 32) + qbase / 32);
+            if (kDrop && p.drop_mask) {
+                // 64 query bits of this key row out of the query-major mask: lane l reads
+                // the words of queries qbase + l and qbase + 32 + l for this warp's 32 keys,
+                // 32 ballot pairs transpose them (lane b keeps key b's query bits)
+                const int W = p.Npad / 32;
+                const uint32_t* mw = p.drop_mask + (static_cast<size_t>(bh) * p.Npad + qbase) * W + kb * 4 + (warp & 3);
+                const uint32_t w0 = mw[static_cast<size_t>(lane) * W], w1 = mw[static_cast<size_t>(lane + 32) * W];
+                uint32_t t0 = 0, t1 = 0;
+#pragma unroll
+                for (int b = 0; b < 32; ++b) {
+                    const uint32_t b0 = __ballot_sync(0xffffffffu, (w0 >> b) & 1u);
+                    const uint32_t b1 = __ballot_sync(0xffffffffu, (w1 >> b) & 1u);
+                    if (lane == b) {
+                        t0 = b0;
+                        t1 = b1;
+                    }
+                }
+                keepm = static_cast<uint64_t>(t0) | (static_cast<uint64_t>(t1) << 32);
             } else if constexpr (kDrop) {
                 // row prefixes of the reference hash for this warpgroup's 64 queries
                 named_bar_sync(1 + h, 128);  // previous step's readers are done

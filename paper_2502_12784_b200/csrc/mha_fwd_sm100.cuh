@@ -37,6 +37,10 @@ struct FwdParams {
     float inv_keep;      // 1 / (1 - dropout_p), binary32 like the reference
     uint64_t drop_seed;
     uint64_t drop_thresh;  // keep iff (hash >> 11) >= drop_thresh
+    // optional: the keep bits as computed, [unit][query][Npad/32] words (bit = key), for
+    // the backward (mha_forward_dropout_mask); nullptr = not kept
+    uint32_t* drop_mask;
+    int mask_words;        // Npad / 32
 };
 
 template <int kD>
@@ -292,6 +296,7 @@ __global__ void __launch_bounds__(384, 1)
             // of quarter q completes (wait::st) while quarter q+1 is computed, so
             // the store latency never sits on the softmax's critical path.
             auto quarter = [&](int qq, uint32_t (&pk)[16], auto poly_pair) {
+                uint32_t kbits = 0;  // keep bits of this quarter's 32 keys
 #pragma unroll
                 for (int x = 0; x < 16; ++x) {
                     const int c = 32 * qq + 2 * x;
@@ -310,9 +315,16 @@ __global__ void __launch_bounds__(384, 1)
                         // (attention_forward.cpp:94-106)
                         const int col = j * 128 + c;
                         const float2 f = unpack2<kBF16>(pk[x]);
-                        pk[x] = pack2<kBF16>(drop_keep(drow, col, p.drop_thresh) ? f.x * p.inv_keep : 0.0f,
-                                             drop_keep(drow, col + 1, p.drop_thresh) ? f.y * p.inv_keep : 0.0f);
+                        const bool k0 = drop_keep(drow, col, p.drop_thresh), k1 = drop_keep(drow, col + 1, p.drop_thresh);
+                        kbits |= (static_cast<uint32_t>(k0) | (static_cast<uint32_t>(k1) << 1)) << (2 * x);
+                        pk[x] = pack2<kBF16>(k0 ? f.x * p.inv_keep : 0.0f, k1 ? f.y * p.inv_keep : 0.0f);
                     }
+                }
+                (void)kbits;
+                if constexpr (kDrop) {
+                    if (p.drop_mask)
+                        p.drop_mask[(static_cast<size_t>(bh) * p.mask_words * 32 + row) * p.mask_words + j * 4 + qq] =
+                            kbits;
                 }
             };
             auto publish = [&](int qq) {  // quarter qq's tcgen05.st has been waited on

@@ -343,3 +343,45 @@ def test_dropout_digest_bitwise_vs_reference(N, br, bc, causal):
     assert vb.dropout_digest(cfg) == ref_digest
     cfg0 = vb.AttnConfig(batch=B, heads=H, seq_len=N, head_dim=d, tile_rows=br, tile_cols=bc, causal=causal)
     assert vb.dropout_digest(cfg0) == 0
+
+
+# ------------------------------------------------- forward-kept dropout mask --
+
+@pytest.mark.parametrize("B,H,N,d,causal,dtype", [(1, 2, 200, 64, True, torch.float16),
+                                                  (2, 1, 384, 128, False, torch.bfloat16),
+                                                  (1, 3, 640, 128, True, torch.bfloat16)])
+def test_forward_dropout_mask_bits_and_backward_bitwise(B, H, N, d, causal, dtype):
+    """mha_forward(drop_mask=...) stores exactly the reference's keep bits of every
+    position it visits (rng.cpp:46-49), and mha_backward(drop_mask=...) reading them is
+    bit-identical to the backward that hashes them itself."""
+    p, seed = 0.15, 4321
+    q, k, v, do = workload(17 + N, (B, H, N, d), dtype)
+    m = torch.zeros(vb.dropout_mask_bytes(q, causal, p), dtype=torch.uint8, device="cuda")
+    o1, l1 = vb.mha_forward(q, k, v, causal, dropout_p=p, seed=seed, drop_mask=m)
+    o0, l0 = vb.mha_forward(q, k, v, causal, dropout_p=p, seed=seed)
+    assert torch.equal(o1, o0) and torch.equal(l1, l0)
+    g1 = vb.mha_backward(q, k, v, o1, do, l1, causal, dropout_p=p, seed=seed, drop_mask=m)
+    g0 = vb.mha_backward(q, k, v, o0, do, l0, causal, dropout_p=p, seed=seed)
+    for name, a, b in zip(("dq", "dk", "dv"), g1, g0):
+        assert torch.equal(a, b), name
+    # the bits themselves, on a sample of rows (bit = key of the query's row words)
+    npad = (N + 127) // 128 * 128
+    words = m.view(torch.int32).view(B * H, npad, npad // 32).cpu().numpy().view(np.uint32)
+    for u in range(B * H):
+        for row in (0, N // 2, N - 1):
+            cols = range(row + 1) if causal else range(N)
+            want = [po.dropout_keep(seed, u // H, u % H, row, c, p) for c in cols]
+            got = [(words[u, row, c // 32] >> (c % 32)) & 1 for c in cols]
+            assert got == [int(x) for x in want], (u, row)
+
+
+def test_autograd_dropout_uses_forward_mask():
+    q, k, v, do = workload(29, (1, 2, 256, 128), torch.bfloat16)
+    qs, ks, vs = (x.clone().requires_grad_(True) for x in (q, k, v))
+    o = vb.attention(qs, ks, vs, causal=True, dropout_p=0.1, seed=99)
+    o.backward(do)
+    ro, rl = vb.mha_forward(q, k, v, True, dropout_p=0.1, seed=99)
+    rg = vb.mha_backward(q, k, v, ro, do, rl, True, dropout_p=0.1, seed=99)
+    assert torch.equal(o.detach(), ro)
+    for a, b in zip((qs.grad, ks.grad, vs.grad), rg):
+        assert torch.equal(a, b)
