@@ -70,12 +70,13 @@ def _load():
     lib.mha_step_host.restype = C.c_int
     lib.vattn_dropout_digest.argtypes = [C.POINTER(_Cfg), C.c_int, C.c_int, vp, vp]
     lib.vattn_dropout_digest.restype = C.c_int
-    lib.mha_dropout_mask_bytes.argtypes = [C.POINTER(_Cfg)]
-    lib.mha_dropout_mask_bytes.restype = C.c_size_t
-    lib.mha_forward_dropout_mask.argtypes = [C.POINTER(_Cfg)] + [vp] * 7
-    lib.mha_forward_dropout_mask.restype = C.c_int
-    lib.mha_backward_dropout_mask.argtypes = [C.POINTER(_Cfg)] + [vp] * 11 + [C.c_size_t, vp]
-    lib.mha_backward_dropout_mask.restype = C.c_int
+    if hasattr(lib, "mha_dropout_mask_bytes"):  # (VATTN_LIB may point at an older build)
+        lib.mha_dropout_mask_bytes.argtypes = [C.POINTER(_Cfg)]
+        lib.mha_dropout_mask_bytes.restype = C.c_size_t
+        lib.mha_forward_dropout_mask.argtypes = [C.POINTER(_Cfg)] + [vp] * 7
+        lib.mha_forward_dropout_mask.restype = C.c_int
+        lib.mha_backward_dropout_mask.argtypes = [C.POINTER(_Cfg)] + [vp] * 11 + [C.c_size_t, vp]
+        lib.mha_backward_dropout_mask.restype = C.c_int
     lib.mha_dpsum.argtypes = [C.POINTER(_Cfg)] + [vp] * 4
     lib.mha_dpsum.restype = C.c_int
     lib.vattn_last_error.restype = C.c_char_p
