@@ -70,7 +70,7 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled (NVML, every 20 ms) during the timed region."""
+    """SM clocks + throttle reasons sampled (NVML, every 10 ms) during the timed region."""
 
     REASONS = {  # nvmlClocksEventReason* bits
         0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
@@ -80,6 +80,7 @@ class ClockSampler:
         self.gpu = gpu_index
         self.samples = []
         self._stop = threading.Event()
+        self._ready = threading.Event()
         self._t = None
 
     def _run(self):
@@ -88,6 +89,7 @@ class ClockSampler:
             nv.nvmlInit()
             h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
             smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self._ready.set()  # NVML is up: the timed region may start
             while not self._stop.is_set():
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 try:
@@ -95,13 +97,18 @@ class ClockSampler:
                 except Exception:
                     r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                 self.samples.append((sm, smax, r))
-                self._stop.wait(0.02)
+                self._stop.wait(0.01)
         except Exception as e:  # sampling is evidence, never fatal
             self.error = str(e)
+        finally:
+            self._ready.set()
 
     def __enter__(self):
+        # NVML import + init can take longer than a short timed region: start sampling
+        # first, and only return (start the clock) once it runs
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._ready.wait(timeout=30)
         return self
 
     def __exit__(self, *a):
