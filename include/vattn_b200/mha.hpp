@@ -335,12 +335,24 @@ inline GradOutputs backward_fused(const std::vector<uint16_t>& q, const std::vec
     detail::upload_padded(bdo.p, d_out.data(), rows, cfg.head_dim, dn, s);
     detail::cuda(cudaMemcpyAsync(blse.p, lse.data(), rows * 4, cudaMemcpyHostToDevice, s), "H2D lse");
     const vattn_config c = detail::to_c(cfg, dn);
-    detail::check(mha_forward(&c, bq.p, bk.p, bv.p, bo.p, static_cast<float*>(bjunk.p), s), "mha_forward");
     const size_t wsb = mha_backward_workspace_bytes(&c);
     detail::DevBuf ws(wsb);
-    detail::check(mha_backward(&c, bq.p, bk.p, bv.p, bo.p, bdo.p, static_cast<const float*>(blse.p),
-                               bdq.p, bdk.p, bdv.p, ws.p, wsb, s),
-                  "mha_backward");
+    if (cfg.dropout_p > 0.0f) {
+        // the recomputed forward keeps its dropout keep bits; the backward reads them
+        // instead of hashing every position again (bit-identical results)
+        detail::DevBuf mask(mha_dropout_mask_bytes(&c));
+        detail::check(mha_forward_dropout_mask(&c, bq.p, bk.p, bv.p, bo.p, static_cast<float*>(bjunk.p), mask.p, s),
+                      "mha_forward_dropout_mask");
+        detail::check(mha_backward_dropout_mask(&c, bq.p, bk.p, bv.p, bo.p, bdo.p, static_cast<const float*>(blse.p),
+                                                mask.p, bdq.p, bdk.p, bdv.p, ws.p, wsb, s),
+                      "mha_backward_dropout_mask");
+        detail::cuda(cudaStreamSynchronize(s), "sync");  // before `mask` is freed
+    } else {
+        detail::check(mha_forward(&c, bq.p, bk.p, bv.p, bo.p, static_cast<float*>(bjunk.p), s), "mha_forward");
+        detail::check(mha_backward(&c, bq.p, bk.p, bv.p, bo.p, bdo.p, static_cast<const float*>(blse.p),
+                                   bdq.p, bdk.p, bdv.p, ws.p, wsb, s),
+                      "mha_backward");
+    }
     GradOutputs g;
     g.traffic = traffic_backward_fused(cfg);
     g.mask_digest = detail::mask_digest(c, cfg.tile_rows, cfg.tile_cols);

@@ -7,7 +7,8 @@
 //
 // Mapping:
 //   vattn::forward_fused       -> vattn_b200::forward_fused (C ABI mha_forward_host)
-//   vattn::backward_fused      -> vattn_b200::backward_fused (mha_forward + mha_backward)
+//   vattn::backward_fused      -> vattn_b200::backward_fused (mha_forward + mha_backward; with dropout
+//                                 the *_dropout_mask pair, the forward keeping its keep bits)
 //   vattn::forward_traditional -> mha_forward_traditional (unfused comparator)
 //   vattn::compute_dpsum       -> mha_dpsum
 //   TrafficCounter             -> closed forms (vattn_b200::traffic_*)
