@@ -207,9 +207,17 @@ def main():
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    # test hook: VATTN_BENCH_SHARED_GPU=1 runs every rank on the visible GPU(s) with gloo
+    # (exercises the N > 1 path on a 1-GPU box; never used for reported numbers)
+    shared = os.environ.get("VATTN_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2502_12784_b200 as vb
 
     B, H, N, d, causal, dt, desc = CONFIGS[args.config]
