@@ -330,8 +330,10 @@ BwdLayout bwd_layout(const vattn_config* c) {
         return e ? atoi(e) : -1;
     }();
     // (the dK/dV kernel's dS^T staging overlaps its dropout row-hash buffer)
-    // d = 64 keeps the recompute path: its shorter dK/dV iterations pay more for the
-    // staging than the dQ GEMM saves (measured: C2 -3 %, C3 at d = 128 +8 %).
+    // d = 64 materialises only for N <= 1024: there the recompute kernel's short
+    // per-CTA loops dominate (N = 512 / 1024: +8 % / +6 %, causal or not); at long N
+    // the shorter dK/dV iterations pay more for the staging than the dQ GEMM saves
+    // (N = 4k / 8k / 16k: -5 / -4 / -7 %).  d = 128: C3 +8 %.
     // Dropout: both backward kernels read the keep bits from a query-major bit mask
     // (BH * Npad^2 / 8 bytes) -- the forward's own (mha_forward_dropout_mask) or one
     // hashed here once -- instead of hashing every position twice.  That also frees the
@@ -345,7 +347,7 @@ BwdLayout bwd_layout(const vattn_config* c) {
     L.drop_mask = c->dropout_p > 0.0f && mask_env;
     L.materialize_ds = c->dropout_p > 0.0f && !L.drop_mask
                            ? false
-                           : (mode_env >= 0 ? mode_env == 1 : (c->head_dim == 128 && ds_bytes <= ds_cap_bytes()));
+                           : (mode_env >= 0 ? mode_env == 1 : ((c->head_dim == 128 || c->seq_len <= 1024) && ds_bytes <= ds_cap_bytes()));
     L.mask = L.ds + (L.materialize_ds ? align256(ds_bytes) : 0);
     L.total = L.mask + (L.drop_mask ? align256(mask_bytes) : 0);
     return L;
