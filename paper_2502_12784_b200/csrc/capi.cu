@@ -329,7 +329,8 @@ BwdLayout bwd_layout(const vattn_config* c) {
         const char* e = getenv("VATTN_DQ_MODE");
         return e ? atoi(e) : -1;
     }();
-    // (the dK/dV kernel's dS^T staging overlaps its dropout row-hash buffer)
+    // (the dK/dV kernel's dS^T staging overlaps its dropout row-hash buffer, used only
+    // when the keep bits are hashed in place)
     // d = 64 materialises only for N <= 1024: there the recompute kernel's short
     // per-CTA loops dominate (N = 512 / 1024: +8 % / +6 %, causal or not); at long N
     // the shorter dK/dV iterations pay more for the staging than the dQ GEMM saves

@@ -156,7 +156,8 @@ struct DkdvCfg {
     static constexpr int kSmemLD = kSmemDO + kStages * kTileBytes;  // [stage][lse2 128 | D 128]
     static constexpr int kSmemDrop = kSmemLD + kStages * 1024;      // dropout row hashes [128] x 16 B
     // dS^T staging for its TMA store (dS materialisation, 2 boxes of 64 queries x 128
-    // keys).  It overlaps the dropout row hashes: materialisation is off with dropout.
+    // keys).  It overlaps the dropout row-hash buffer, which is only used when dropout
+    // bits are hashed in place (no keep-bit mask) -- and then materialisation is off.
     static constexpr int kSmemDsStage = kSmemDrop;
     static constexpr int kSmemBar = kSmemDsStage + 32768;
     static constexpr int kNumBars = 16;
