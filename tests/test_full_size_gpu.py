@@ -76,3 +76,22 @@ def test_every_unit_equals_its_one_unit_slab(shape, causal):
         assert torch.equal(o1, flat[4][u:u + 1]) and torch.equal(l1, lse_f[u:u + 1]), u
         for name, a, r in zip(("dq", "dk", "dv"), g1, flat[5:]):
             assert torch.equal(a, r[u:u + 1]), (name, u)
+
+
+def test_full_size_dropout_mask_paths_bitwise():
+    """C3 with dropout p = 0.1 (the paper's benchmark setting): the forward-kept keep-bit
+    mask and the backward's own mask kernel give bit-identical gradients, run to run."""
+    B, H, N, d, causal, p, seed = 4, 16, 8192, 128, True, 0.1, 31337
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    q, k, v, do = (torch.randn((B, H, N, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+    m = torch.empty(vb.dropout_mask_bytes(q, causal, p), dtype=torch.uint8, device="cuda")
+    o1, l1 = vb.mha_forward(q, k, v, causal, dropout_p=p, seed=seed, drop_mask=m)
+    g1 = vb.mha_backward(q, k, v, o1, do, l1, causal, dropout_p=p, seed=seed, drop_mask=m)
+    o2, l2 = vb.mha_forward(q, k, v, causal, dropout_p=p, seed=seed)
+    g2 = vb.mha_backward(q, k, v, o2, do, l2, causal, dropout_p=p, seed=seed)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    for name, a, b in zip(("dq", "dk", "dv"), g1, g2):
+        assert torch.equal(a, b), name
+        assert torch.isfinite(a.float()).all(), name
