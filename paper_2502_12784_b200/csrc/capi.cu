@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -218,12 +219,14 @@ int dkdv_tail_units(int BH, int n_q) {
         const char* e = getenv("VATTN_DKDV_TAIL_WAVES");
         return e ? atof(e) : 3.5;
     }();
-    static int sm_count[64] = {};  // per device, queried once
+    static std::atomic<int> sm_count[64] = {};  // per device; racing writers store the same value
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
-    if (!sm_count[dev] && cudaDeviceGetAttribute(&sm_count[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-        sm_count[dev] = 148;
-    const int sms = sm_count[dev];
+    int sms = sm_count[dev].load(std::memory_order_relaxed);
+    if (!sms) {
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+        sm_count[dev].store(sms, std::memory_order_relaxed);
+    }
     const int T = static_cast<int>((waves * sms + n_q - 1) / n_q);
     return T < 0 ? 0 : (T > BH ? BH : T);
 }
@@ -302,14 +305,16 @@ struct BwdLayout {
 // (57.8 vs 62.6 ms); on 8 GPUs each shard needs 8.6 GB.  VATTN_DQ_MODE=0/1 forces a
 // mode (tuning and tests).
 size_t ds_cap_bytes() {
-    static size_t cap[64] = {};
+    static std::atomic<size_t> cap[64] = {};  // per device; racing writers store the same value
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
-    if (!cap[dev]) {
+    size_t c = cap[dev].load(std::memory_order_relaxed);
+    if (!c) {
         size_t free_b = 0, total_b = 0;
-        cap[dev] = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess ? total_b / 5 * 2 : (32ull << 30);
+        c = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess ? total_b / 5 * 2 : (32ull << 30);
+        cap[dev].store(c, std::memory_order_relaxed);
     }
-    return cap[dev];
+    return c;
 }
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
