@@ -382,12 +382,17 @@ def backward_fused(q, k, v, d_out, lse, cfg: AttnConfig, out=None):
     reference (attention_backward.cpp:91-104) it recomputes O with the forward
     when ``out`` is not given."""
     (qp, kp, vp, dop), dn = _prep(cfg, q, k, v, d_out)
+    mask = None
     if out is None:
-        op, _ = mha_forward(qp, kp, vp, cfg.causal, cfg.scale(), dropout_p=cfg.dropout_p, seed=cfg.seed)
+        if cfg.dropout_p > 0.0:  # the recomputed forward keeps its keep bits for the backward
+            mask = torch.empty(dropout_mask_bytes(qp, cfg.causal, cfg.dropout_p), dtype=torch.uint8,
+                               device=qp.device)
+        op, _ = mha_forward(qp, kp, vp, cfg.causal, cfg.scale(), dropout_p=cfg.dropout_p, seed=cfg.seed,
+                            drop_mask=mask)
     else:
         op = _pad(out.contiguous(), dn)
     dq, dk, dv = mha_backward(qp, kp, vp, op, dop, lse.contiguous(), cfg.causal, cfg.scale(),
-                              dropout_p=cfg.dropout_p, seed=cfg.seed)
+                              dropout_p=cfg.dropout_p, seed=cfg.seed, drop_mask=mask)
     d = cfg.head_dim
     return dq[..., :d].contiguous(), dk[..., :d].contiguous(), dv[..., :d].contiguous()
 
