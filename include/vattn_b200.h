@@ -21,7 +21,10 @@
  *     host threads on different streams.
  *   - Every call returns a vattn_status; on failure vattn_last_error() returns a
  *     thread-local message.  VATTN_EINVAL corresponds to the reference's
- *     std::invalid_argument, VATTN_EDOMAIN to std::domain_error.
+ *     std::invalid_argument, VATTN_EDOMAIN to std::domain_error (a query row with
+ *     a NaN / +inf score or an empty softmax sum, online_softmax.cpp:33-34, 81-82):
+ *     the synchronous host entry points return it; the asynchronous device entry
+ *     points report it through the optional status word of mha_forward_ex.
  *   - head_dim must be 64 or 128 at this boundary (the C++ layer
  *     include/vattn_b200/mha.hpp zero-pads other head dims); any seq_len >= 1.
  *   - No CPU fallback: when the sm_100a kernels cannot run, calls fail with
@@ -48,7 +51,7 @@
 extern "C" {
 #endif
 
-#define VATTN_B200_ABI_VERSION 3
+#define VATTN_B200_ABI_VERSION 4
 
 typedef enum vattn_status {
     VATTN_OK = 0,
@@ -87,8 +90,25 @@ typedef struct vattn_config {
 int mha_forward(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o,
                 float* lse, void* stream);
 
+/* mha_forward with the two optional extras (replaces the reference's forward_fused
+ * checks, attention_forward.cpp:191-227 -> online_softmax.cpp:33-34, 81-82):
+ *   drop_mask  as mha_forward_dropout_mask (NULL = do not keep the keep bits);
+ *   status     device word (4-byte aligned, zeroed by the caller) into which the
+ *              kernel ORs VATTN_DOMAIN_ROW when any query row had a NaN or +inf
+ *              score or an empty softmax sum (l == 0) -- the rows for which the
+ *              reference throws std::domain_error.  NULL = unchecked.  Reading it
+ *              after the stream synchronises is the caller's domain check. */
+#define VATTN_DOMAIN_ROW 1u
+int mha_forward_ex(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o, float* lse,
+                   void* drop_mask, unsigned int* status, void* stream);
+
 /* Bytes of device workspace mha_backward needs for `cfg` (0 on invalid cfg). */
 size_t mha_backward_workspace_bytes(const vattn_config* cfg);
+
+/* Bytes of workspace mha_backward_dropout_mask needs: the caller's keep-bit mask
+ * replaces the workspace's own mask region (equal to mha_backward_workspace_bytes
+ * without dropout). */
+size_t mha_backward_workspace_bytes_mask(const vattn_config* cfg);
 
 /* dQ, dK, dV of the forward above given dO, O and lse.  `workspace` must hold
  * mha_backward_workspace_bytes(cfg) bytes (256-byte aligned); its contents on
@@ -100,7 +120,8 @@ int mha_backward(const vattn_config* cfg, const void* q, const void* k, const vo
 
 /* Dropout keep bits kept from the forward for the backward (optional fast path).
  * mha_dropout_mask_bytes(cfg): size of the mask, B*H*Npad*Npad/8 bytes with Npad = N
- * rounded up to 128 (0 when dropout_p == 0 or cfg is invalid).
+ * rounded up to 128 (0 when dropout_p == 0, cfg is invalid, or masks are disabled
+ * with VATTN_DROP_MASK=0 -- then both backward kernels hash the bits in place).
  * mha_forward_dropout_mask: mha_forward that also stores the keep bits it computes
  * (query-major, one bit per (query, key) position it visits) into `drop_mask`.
  * mha_backward_dropout_mask: mha_backward that reads those bits instead of hashing
@@ -140,7 +161,8 @@ int vattn_dropout_digest(const vattn_config* cfg, int tile_rows, int tile_cols, 
  * vattn::forward_fused / backward_fused).  Results are bit-identical to the
  * device entry points. */
 
-/* vattn::forward_fused on host buffers: O, lse. */
+/* vattn::forward_fused on host buffers: O, lse.  Returns VATTN_EDOMAIN where the
+ * reference throws std::domain_error (see mha_forward_ex). */
 int mha_forward_host(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o,
                      float* lse, void* stream);
 
@@ -150,7 +172,8 @@ int mha_backward_host(const vattn_config* cfg, const void* q, const void* k, con
                       void* dv, void* stream);
 
 /* One attention training step on host buffers: forward then backward with Q, K,
- * V and dO crossing PCIe once, O, lse, dQ, dK, dV returned. */
+ * V and dO crossing PCIe once, O, lse, dQ, dK, dV returned.  VATTN_EDOMAIN as
+ * mha_forward_host. */
 int mha_step_host(const vattn_config* cfg, const void* q, const void* k, const void* v,
                   const void* dout, void* o, float* lse, void* dq, void* dk, void* dv,
                   void* stream);
@@ -163,6 +186,10 @@ int vattn_abi_version(void);
 
 /* Number of kernels the last successful call on this thread launched. */
 int vattn_last_launch_count(void);
+
+/* TMA descriptor cache counters (tensor maps are cached per pointer, shape and
+ * dtype): lookups served from the cache and maps encoded. */
+void vattn_map_cache_stats(long long* hits, long long* misses);
 
 /* Measurement hooks (bench / roofline only; off by default).  When enabled,
  * every call records CUDA events on its stream around the hot kernels;

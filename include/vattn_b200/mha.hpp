@@ -204,6 +204,22 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
 };
 
+// Device domain-error word of one call (mha_forward_ex): zeroed on creation;
+// throw_if_set() -- after the stream synchronised -- throws std::domain_error where
+// the reference does (online_softmax.cpp:33-34 NaN score, :81-82 l == 0).
+struct DomainWord {
+    DevBuf buf{sizeof(unsigned int)};
+    explicit DomainWord(cudaStream_t s) { cuda(cudaMemsetAsync(buf.p, 0, sizeof(unsigned int), s), "memset"); }
+    unsigned int* ptr() const { return static_cast<unsigned int*>(buf.p); }
+    void throw_if_set(const char* where) const {
+        unsigned int h = 0;
+        cuda(cudaMemcpy(&h, buf.p, sizeof(h), cudaMemcpyDeviceToHost), "D2H status");
+        if (h & VATTN_DOMAIN_ROW)
+            throw std::domain_error(std::string(where) +
+                                    ": softmax: NaN score or fully masked row (l == 0) in a query row");
+    }
+};
+
 inline int native_dim(int d) {
     if (d <= 64) return 64;
     if (d <= 128) return 128;
@@ -256,13 +272,16 @@ inline uint64_t mask_digest(const vattn_config& c, int tile_rows, int tile_cols)
 
 // ---------------------------------------------------------- device overloads
 
+// `status` (optional): zeroed device word that receives VATTN_DOMAIN_ROW for the rows
+// where the reference would throw std::domain_error (read it after synchronising).
 inline void forward_fused_device(const AttnConfig& cfg, const void* q, const void* k, const void* v,
-                                 void* out, float* lse, cudaStream_t stream = nullptr) {
+                                 void* out, float* lse, cudaStream_t stream = nullptr,
+                                 unsigned int* status = nullptr) {
     cfg.validate();
     if (cfg.head_dim != 64 && cfg.head_dim != 128)
         throw std::invalid_argument("forward_fused_device: head_dim must be 64 or 128 (use the host overload to pad)");
     const vattn_config c = detail::to_c(cfg, cfg.head_dim);
-    detail::check(mha_forward(&c, q, k, v, out, lse, stream), "mha_forward");
+    detail::check(mha_forward_ex(&c, q, k, v, out, lse, nullptr, status, stream), "mha_forward_ex");
 }
 
 inline void backward_fused_device(const AttnConfig& cfg, const void* q, const void* k,
@@ -306,10 +325,13 @@ inline ForwardOutput forward_fused(const std::vector<uint16_t>& q, const std::ve
     detail::upload_padded(dq.p, q.data(), rows, cfg.head_dim, dn, s);
     detail::upload_padded(dk.p, k.data(), rows, cfg.head_dim, dn, s);
     detail::upload_padded(dv.p, v.data(), rows, cfg.head_dim, dn, s);
-    detail::check(mha_forward(&c, dq.p, dk.p, dv.p, dout.p, static_cast<float*>(dlse.p), s), "mha_forward");
+    detail::DomainWord dom(s);
+    detail::check(mha_forward_ex(&c, dq.p, dk.p, dv.p, dout.p, static_cast<float*>(dlse.p), nullptr, dom.ptr(), s),
+                  "mha_forward_ex");
     detail::download_padded(r.out.data(), dout.p, rows, cfg.head_dim, dn, s);
     detail::cuda(cudaMemcpyAsync(r.lse.data(), dlse.p, rows * 4, cudaMemcpyDeviceToHost, s), "D2H lse");
     detail::cuda(cudaStreamSynchronize(s), "sync");
+    dom.throw_if_set("forward_fused");
     return r;
 }
 
@@ -335,24 +357,33 @@ inline GradOutputs backward_fused(const std::vector<uint16_t>& q, const std::vec
     detail::upload_padded(bdo.p, d_out.data(), rows, cfg.head_dim, dn, s);
     detail::cuda(cudaMemcpyAsync(blse.p, lse.data(), rows * 4, cudaMemcpyHostToDevice, s), "H2D lse");
     const vattn_config c = detail::to_c(cfg, dn);
-    const size_t wsb = mha_backward_workspace_bytes(&c);
-    detail::DevBuf ws(wsb);
-    if (cfg.dropout_p > 0.0f) {
+    // the recomputed forward (as the reference's) raises the reference's domain errors
+    detail::DomainWord dom(s);
+    const size_t mask_bytes = cfg.dropout_p > 0.0f ? mha_dropout_mask_bytes(&c) : 0;
+    if (mask_bytes) {
         // the recomputed forward keeps its dropout keep bits; the backward reads them
-        // instead of hashing every position again (bit-identical results)
-        detail::DevBuf mask(mha_dropout_mask_bytes(&c));
-        detail::check(mha_forward_dropout_mask(&c, bq.p, bk.p, bv.p, bo.p, static_cast<float*>(bjunk.p), mask.p, s),
-                      "mha_forward_dropout_mask");
+        // instead of hashing every position again (bit-identical results), so the
+        // workspace needs no mask region of its own
+        const size_t wsb = mha_backward_workspace_bytes_mask(&c);
+        detail::DevBuf ws(wsb);
+        detail::DevBuf mask(mask_bytes);
+        detail::check(mha_forward_ex(&c, bq.p, bk.p, bv.p, bo.p, static_cast<float*>(bjunk.p), mask.p, dom.ptr(), s),
+                      "mha_forward_ex");
         detail::check(mha_backward_dropout_mask(&c, bq.p, bk.p, bv.p, bo.p, bdo.p, static_cast<const float*>(blse.p),
                                                 mask.p, bdq.p, bdk.p, bdv.p, ws.p, wsb, s),
                       "mha_backward_dropout_mask");
         detail::cuda(cudaStreamSynchronize(s), "sync");  // before `mask` is freed
     } else {
-        detail::check(mha_forward(&c, bq.p, bk.p, bv.p, bo.p, static_cast<float*>(bjunk.p), s), "mha_forward");
+        const size_t wsb = mha_backward_workspace_bytes(&c);
+        detail::DevBuf ws(wsb);
+        detail::check(mha_forward_ex(&c, bq.p, bk.p, bv.p, bo.p, static_cast<float*>(bjunk.p), nullptr, dom.ptr(), s),
+                      "mha_forward_ex");
         detail::check(mha_backward(&c, bq.p, bk.p, bv.p, bo.p, bdo.p, static_cast<const float*>(blse.p),
                                    bdq.p, bdk.p, bdv.p, ws.p, wsb, s),
                       "mha_backward");
+        detail::cuda(cudaStreamSynchronize(s), "sync");  // before `ws` is freed
     }
+    dom.throw_if_set("backward_fused");
     GradOutputs g;
     g.traffic = traffic_backward_fused(cfg);
     g.mask_digest = detail::mask_digest(c, cfg.tile_rows, cfg.tile_cols);

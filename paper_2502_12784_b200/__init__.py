@@ -79,6 +79,13 @@ def _load():
         lib.mha_backward_dropout_mask.restype = C.c_int
     lib.mha_dpsum.argtypes = [C.POINTER(_Cfg)] + [vp] * 4
     lib.mha_dpsum.restype = C.c_int
+    if hasattr(lib, "mha_forward_ex"):  # ABI >= 4
+        lib.mha_forward_ex.argtypes = [C.POINTER(_Cfg)] + [vp] * 8
+        lib.mha_forward_ex.restype = C.c_int
+        lib.mha_backward_workspace_bytes_mask.argtypes = [C.POINTER(_Cfg)]
+        lib.mha_backward_workspace_bytes_mask.restype = C.c_size_t
+        lib.vattn_map_cache_stats.argtypes = [C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]
+        lib.vattn_map_cache_stats.restype = None
     lib.vattn_last_error.restype = C.c_char_p
     lib.vattn_abi_version.restype = C.c_int
     lib.vattn_last_launch_count.restype = C.c_int
@@ -173,8 +180,26 @@ def _check(ts, shape, dtype, names):
             raise ValueError(f"{n} must be contiguous [B, H, N, d]")
 
 
-def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def _stream(dev=None) -> int:
+    """The current stream of `dev` (the tensors' device), not of the current device."""
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _check_out(t, shape, dtype, name, dev):
+    """Caller-supplied output buffer: the kernels write every element of `shape`."""
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+        raise ValueError(f"{name}: expected {dtype} {tuple(shape)}, got {t.dtype} {tuple(t.shape)}")
+    if not t.is_cuda or t.device != dev:
+        raise ValueError(f"{name} must be a CUDA tensor on {dev}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _domain_check(status: torch.Tensor, where: str):
+    """Synchronises on the status word; the reference throws std::domain_error here."""
+    if int(status.item()) & 1:
+        raise ArithmeticError(f"{where}: softmax: NaN score or fully masked row (l == 0) in a query row "
+                              "(reference: std::domain_error, online_softmax.cpp:33-34 / 81-82)")
 
 
 def _native_dim(d: int) -> int:
@@ -190,24 +215,41 @@ def _pad(t: torch.Tensor, dn: int) -> torch.Tensor:
 
 
 def mha_forward(q, k, v, causal: bool = False, softmax_scale: float = 0.0, out=None, lse=None,
-                dropout_p: float = 0.0, seed: int = 0, bh_slab=None, drop_mask=None):
+                dropout_p: float = 0.0, seed: int = 0, bh_slab=None, drop_mask=None, check_domain: bool = False):
     """C ABI ``mha_forward`` on CUDA tensors [B, H, N, d] (d in {64, 128}).
     Returns (out, lse) with lse [B, H, N] fp32 natural-log.  ``dropout_p > 0``
-    applies the reference's dropout (keep bits = vattn::dropout_keep(seed, b, h, row, col, p))."""
+    applies the reference's dropout (keep bits = vattn::dropout_keep(seed, b, h, row, col, p)).
+    ``check_domain``: synchronise and raise ArithmeticError where the reference throws
+    std::domain_error (a NaN / +inf score or an empty softmax row; C ABI mha_forward_ex)."""
     _check((q, k, v), q.shape, q.dtype, ("q", "k", "v"))
     B, H, N, d = q.shape
-    out = torch.empty_like(q) if out is None else out
-    lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
-    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
-    if drop_mask is not None:  # also keep the dropout keep bits for mha_backward(drop_mask=...)
-        _check_mask(drop_mask, cfg)
-        rc = lib.mha_forward_dropout_mask(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                                          lse.data_ptr(), drop_mask.data_ptr(), _stream())
+    dev = q.device
+    if out is None:
+        out = torch.empty_like(q)
     else:
-        rc = lib.mha_forward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                             lse.data_ptr(), _stream())
+        _check_out(out, q.shape, q.dtype, "out", dev)
+    if lse is None:
+        lse = torch.empty((B, H, N), dtype=torch.float32, device=dev)
+    else:
+        _check_out(lse, (B, H, N), torch.float32, "lse", dev)
+    cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
+    status = None
+    with torch.cuda.device(dev):
+        if drop_mask is not None:  # also keep the dropout keep bits for mha_backward(drop_mask=...)
+            _check_mask(drop_mask, cfg)
+        if check_domain:
+            status = torch.zeros(1, dtype=torch.int32, device=dev)
+        if drop_mask is not None or check_domain:
+            rc = lib.mha_forward_ex(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                    lse.data_ptr(), None if drop_mask is None else drop_mask.data_ptr(),
+                                    None if status is None else status.data_ptr(), _stream(dev))
+        else:
+            rc = lib.mha_forward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                 lse.data_ptr(), _stream(dev))
     if rc:
         _raise(rc, "mha_forward")
+    if status is not None:
+        _domain_check(status, "mha_forward")
     return out, lse
 
 
@@ -218,15 +260,28 @@ def dropout_mask_bytes(q, causal: bool = False, dropout_p: float = 0.0, bh_slab=
 
 def _check_mask(m, cfg):
     need = int(lib.mha_dropout_mask_bytes(C.byref(cfg)))
+    if need == 0:
+        raise ValueError("drop_mask given but keep-bit masks are off (dropout_p == 0 or VATTN_DROP_MASK=0)")
     if not m.is_cuda or m.numel() * m.element_size() < need or m.data_ptr() % 256:
         raise ValueError(f"drop_mask must be a 256-byte aligned CUDA buffer of >= {need} bytes")
 
 
-def workspace_bytes(B, H, N, d, causal=False, dtype=torch.float16, dropout_p: float = 0.0) -> int:
-    """mha_backward workspace (dropout adds the keep-bit masks)."""
+def workspace_bytes(B, H, N, d, causal=False, dtype=torch.float16, dropout_p: float = 0.0,
+                    external_mask: bool = False) -> int:
+    """mha_backward workspace.  With dropout it includes a keep-bit mask region unless
+    ``external_mask`` (the caller passes the forward's mask: mha_backward(drop_mask=...))."""
     cfg = _Cfg(B, H, N, d, 1 if causal else 0, 0.0, VATTN_BF16 if dtype == torch.bfloat16 else VATTN_F16,
                float(dropout_p), 0, 0, 0)
+    if external_mask:
+        return int(lib.mha_backward_workspace_bytes_mask(C.byref(cfg)))
     return int(lib.mha_backward_workspace_bytes(C.byref(cfg)))
+
+
+def keep_mask_cap_bytes() -> int:
+    """Largest keep-bit mask the autograd binding / backward_fused keep from forward to
+    backward (VATTN_KEEP_MASK_MB, default 2048 MiB).  Larger masks are not kept: the
+    backward then hashes the bits itself into its (transient) workspace."""
+    return int(float(os.environ.get("VATTN_KEEP_MASK_MB", "2048")) * (1 << 20))
 
 
 def mha_backward(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: float = 0.0,
@@ -239,26 +294,38 @@ def mha_backward(q, k, v, o, dout, lse, causal: bool = False, softmax_scale: flo
     B, H, N, d = q.shape
     if lse.shape != (B, H, N) or lse.dtype != torch.float32 or not lse.is_contiguous():
         raise ValueError("lse must be a contiguous float32 [B, H, N] tensor")
+    dev = q.device
+    if lse.device != dev:
+        raise ValueError(f"lse must be on {dev}")
     cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
-    need = int(lib.mha_backward_workspace_bytes(C.byref(cfg)))
+    need = int(lib.mha_backward_workspace_bytes(C.byref(cfg)) if drop_mask is None
+               else lib.mha_backward_workspace_bytes_mask(C.byref(cfg)))
     if need == 0:
         rc = lib.mha_backward(C.byref(cfg), *([None] * 10), 0, None)
         _raise(rc if rc else VATTN_EINVAL, "mha_backward")
     if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
-    dq = torch.empty_like(q) if dq is None else dq
-    dk = torch.empty_like(q) if dk is None else dk
-    dv = torch.empty_like(q) if dv is None else dv
-    if drop_mask is not None:  # the forward's keep bits (mha_forward(drop_mask=...))
-        _check_mask(drop_mask, cfg)
-        rc = lib.mha_backward_dropout_mask(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
-                                           dout.data_ptr(), lse.data_ptr(), drop_mask.data_ptr(), dq.data_ptr(),
-                                           dk.data_ptr(), dv.data_ptr(), workspace.data_ptr(), workspace.numel(),
-                                           _stream())
-    else:
-        rc = lib.mha_backward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
-                              dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
-                              workspace.data_ptr(), workspace.numel(), _stream())
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    elif not workspace.is_cuda or workspace.device != dev or not workspace.is_contiguous():
+        raise ValueError(f"workspace must be a contiguous CUDA buffer on {dev}")
+    grads = []
+    for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+        if t is None:
+            t = torch.empty_like(q)
+        else:
+            _check_out(t, q.shape, q.dtype, n, dev)
+        grads.append(t)
+    dq, dk, dv = grads
+    with torch.cuda.device(dev):
+        if drop_mask is not None:  # the forward's keep bits (mha_forward(drop_mask=...))
+            _check_mask(drop_mask, cfg)
+            rc = lib.mha_backward_dropout_mask(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                               dout.data_ptr(), lse.data_ptr(), drop_mask.data_ptr(), dq.data_ptr(),
+                                               dk.data_ptr(), dv.data_ptr(), workspace.data_ptr(),
+                                               workspace.numel() * workspace.element_size(), _stream(dev))
+        else:
+            rc = lib.mha_backward(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                  dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                                  workspace.data_ptr(), workspace.numel() * workspace.element_size(), _stream(dev))
     if rc:
         _raise(rc, "mha_backward")
     return dq, dk, dv
@@ -287,6 +354,8 @@ def mha_forward_host(q, k, v, causal: bool = False, softmax_scale: float = 0.0, 
     B, H, N, d = q.shape
     out = _host_empty(q.shape, q.dtype, q) if out is None else out
     lse = _host_empty((B, H, N), torch.float32, q) if lse is None else lse
+    _check_host((out,), q.shape, q.dtype, ("out",))
+    _check_host((lse,), (B, H, N), torch.float32, ("lse",))
     cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
     rc = lib.mha_forward_host(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                               lse.data_ptr(), _stream())
@@ -302,6 +371,7 @@ def mha_backward_host(q, k, v, o, dout, lse, causal: bool = False, softmax_scale
     B, H, N, d = q.shape
     _check_host((lse,), (B, H, N), torch.float32, ("lse",))
     dq, dk, dv = (_host_empty(q.shape, q.dtype, q) if t is None else t for t in (dq, dk, dv))
+    _check_host((dq, dk, dv), q.shape, q.dtype, ("dq", "dk", "dv"))
     cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
     rc = lib.mha_backward_host(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                dout.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
@@ -322,6 +392,8 @@ def mha_step_host(q, k, v, dout, causal: bool = False, softmax_scale: float = 0.
         out = (_host_empty(q.shape, q.dtype, q), _host_empty((B, H, N), torch.float32, q),
                *(_host_empty(q.shape, q.dtype, q) for _ in range(3)))
     o, lse, dq, dk, dv = out
+    _check_host((o, dq, dk, dv), q.shape, q.dtype, ("o", "dq", "dk", "dv"))
+    _check_host((lse,), (B, H, N), torch.float32, ("lse",))
     cfg = _cfg(q, causal, softmax_scale, dropout_p, seed, bh_slab)
     rc = lib.mha_step_host(C.byref(cfg), q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), o.data_ptr(),
                            lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), _stream())
@@ -337,7 +409,8 @@ def compute_dpsum(d_out, out):
     B, H, N, d = out.shape
     D = torch.empty((B, H, N), dtype=torch.float32, device=out.device)
     cfg = _cfg(out, False, 0.0)
-    rc = lib.mha_dpsum(C.byref(cfg), out.data_ptr(), d_out.data_ptr(), D.data_ptr(), _stream())
+    with torch.cuda.device(out.device):
+        rc = lib.mha_dpsum(C.byref(cfg), out.data_ptr(), d_out.data_ptr(), D.data_ptr(), _stream(out.device))
     if rc:
         _raise(rc, "mha_dpsum")
     return D
@@ -373,7 +446,8 @@ def forward_fused(q, k, v, cfg: AttnConfig):
     """vattn::forward_fused on CUDA tensors: returns (out, lse).  head_dim other
     than 64/128 is zero-padded (exact: padded columns add 0 to every dot product)."""
     (qp, kp, vp), dn = _prep(cfg, q, k, v)
-    out, lse = mha_forward(qp, kp, vp, cfg.causal, cfg.scale(), dropout_p=cfg.dropout_p, seed=cfg.seed)
+    out, lse = mha_forward(qp, kp, vp, cfg.causal, cfg.scale(), dropout_p=cfg.dropout_p, seed=cfg.seed,
+                           check_domain=True)
     return out[..., : cfg.head_dim].contiguous(), lse
 
 
@@ -384,11 +458,11 @@ def backward_fused(q, k, v, d_out, lse, cfg: AttnConfig, out=None):
     (qp, kp, vp, dop), dn = _prep(cfg, q, k, v, d_out)
     mask = None
     if out is None:
-        if cfg.dropout_p > 0.0:  # the recomputed forward keeps its keep bits for the backward
-            mask = torch.empty(dropout_mask_bytes(qp, cfg.causal, cfg.dropout_p), dtype=torch.uint8,
-                               device=qp.device)
+        mb = dropout_mask_bytes(qp, cfg.causal, cfg.dropout_p)
+        if 0 < mb <= keep_mask_cap_bytes():  # the recomputed forward keeps its keep bits for the backward
+            mask = torch.empty(mb, dtype=torch.uint8, device=qp.device)
         op, _ = mha_forward(qp, kp, vp, cfg.causal, cfg.scale(), dropout_p=cfg.dropout_p, seed=cfg.seed,
-                            drop_mask=mask)
+                            drop_mask=mask, check_domain=True)
     else:
         op = _pad(out.contiguous(), dn)
     dq, dk, dv = mha_backward(qp, kp, vp, op, dop, lse.contiguous(), cfg.causal, cfg.scale(),
@@ -407,20 +481,27 @@ class MHAFunction(torch.autograd.Function):
         qp, kp, vp = (_pad(x.contiguous(), dn) for x in (q, k, v))
         scale = softmax_scale if softmax_scale > 0 else 1.0 / math.sqrt(d)
         mask = None
-        if dropout_p > 0.0:  # keep the forward's keep bits: the backward skips re-hashing them
-            mask = torch.empty(dropout_mask_bytes(qp, causal, dropout_p), dtype=torch.uint8, device=qp.device)
+        mb = dropout_mask_bytes(qp, causal, dropout_p)
+        if 0 < mb <= keep_mask_cap_bytes():
+            # keep the forward's keep bits: the backward skips re-hashing them (a bigger
+            # mask is not kept -- the backward hashes the bits into its own workspace)
+            mask = torch.empty(mb, dtype=torch.uint8, device=qp.device)
         o, lse = mha_forward(qp, kp, vp, causal, scale, dropout_p=dropout_p, seed=seed, drop_mask=mask)
-        ctx.save_for_backward(qp, kp, vp, o, lse)
-        ctx.drop_mask = mask
+        if mask is not None:
+            ctx.save_for_backward(qp, kp, vp, o, lse, mask)
+        else:
+            ctx.save_for_backward(qp, kp, vp, o, lse)
         ctx.causal, ctx.scale, ctx.d, ctx.dropout_p, ctx.seed = causal, scale, d, dropout_p, seed
         return o[..., :d] if dn != d else o
 
     @staticmethod
     def backward(ctx, do):
-        qp, kp, vp, o, lse = ctx.saved_tensors
+        saved = ctx.saved_tensors
+        qp, kp, vp, o, lse = saved[:5]
+        mask = saved[5] if len(saved) > 5 else None
         dop = _pad(do.contiguous(), qp.shape[-1])
         dq, dk, dv = mha_backward(qp, kp, vp, o, dop, lse, ctx.causal, ctx.scale,
-                                  dropout_p=ctx.dropout_p, seed=ctx.seed, drop_mask=ctx.drop_mask)
+                                  dropout_p=ctx.dropout_p, seed=ctx.seed, drop_mask=mask)
         d = ctx.d
         return dq[..., :d], dk[..., :d], dv[..., :d], None, None, None, None
 

@@ -84,8 +84,53 @@ EncodeFn encode_fn() {
     return fn;
 }
 
+// Encoded tensor maps, cached per (kind, pointer, shape, dtype): a map is
+// a pure function of those values, so a hit is exact even when the memory behind the
+// pointer was freed and reallocated.  Encoding costs ~1-2 us of host time per map and
+// a call needs 4-6 of them, which matters for launch-bound configs (C1, C4).
+// Direct-mapped, 256 entries, one mutex (lookups are ~100 ns).
+struct MapKey {
+    int kind;  // 0 = [BH, N, d] operand, 1 = dS^T scratch
+    const void* ptr;
+    long long a, b, c;
+    bool bf16;
+    bool operator==(const MapKey& o) const {
+        return kind == o.kind && ptr == o.ptr && a == o.a && b == o.b && c == o.c && bf16 == o.bf16;
+    }
+};
+struct MapCache {
+    static constexpr int kSlots = 256;
+    std::mutex mu;
+    MapKey key[kSlots];
+    CUtensorMap map[kSlots];
+    bool used[kSlots] = {};
+    static size_t slot(const MapKey& k) {
+        size_t h = reinterpret_cast<uintptr_t>(k.ptr) >> 8;
+        h ^= static_cast<size_t>(k.a) * 0x9E3779B97F4A7C15ull ^ static_cast<size_t>(k.b) * 0xC2B2AE3D27D4EB4Full ^
+             static_cast<size_t>(k.c) * 0x165667B19E3779F9ull ^ static_cast<size_t>(k.kind * 2 + k.bf16);
+        h ^= h >> 29;
+        return h % kSlots;
+    }
+    bool get(const MapKey& k, CUtensorMap* out) {
+        std::lock_guard<std::mutex> l(mu);
+        const size_t s = slot(k);
+        if (!used[s] || !(key[s] == k)) return false;
+        *out = map[s];
+        return true;
+    }
+    void put(const MapKey& k, const CUtensorMap& m) {
+        std::lock_guard<std::mutex> l(mu);
+        const size_t s = slot(k);
+        key[s] = k;
+        map[s] = m;
+        used[s] = true;
+    }
+};
+MapCache g_maps;
+std::atomic<long long> g_map_hits{0}, g_map_misses{0};
+
 // [B*H, N, d] 16-bit tensor, 128 rows x 64 columns per box, 128-byte swizzle.
-bool make_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16) {
+bool encode_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16) {
     EncodeFn enc = encode_fn();
     if (!enc) return false;
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(N),
@@ -102,8 +147,20 @@ bool make_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16) 
     return r == CUDA_SUCCESS;
 }
 
+bool make_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16) {
+    const MapKey k{0, ptr, BH, N, D, bf16};
+    if (g_maps.get(k, m)) {
+        g_map_hits.fetch_add(1, std::memory_order_relaxed);
+        return true;
+    }
+    g_map_misses.fetch_add(1, std::memory_order_relaxed);
+    if (!encode_map(m, ptr, BH, N, D, bf16)) return false;
+    g_maps.put(k, *m);
+    return true;
+}
+
 // dS^T scratch viewed as [tiles][128 keys][128 queries] 16-bit, 64-query x 128-key boxes.
-bool make_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16) {
+bool encode_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16) {
     EncodeFn enc = encode_fn();
     if (!enc || tiles > (1ll << 31) - 1) return false;
     const cuuint64_t dims[3] = {128, 128, static_cast<cuuint64_t>(tiles)};
@@ -113,6 +170,18 @@ bool make_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16) {
     return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(ptr),
                dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool make_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16) {
+    const MapKey k{1, ptr, tiles, 0, 0, bf16};
+    if (g_maps.get(k, m)) {
+        g_map_hits.fetch_add(1, std::memory_order_relaxed);
+        return true;
+    }
+    g_map_misses.fetch_add(1, std::memory_order_relaxed);
+    if (!encode_ds_map(m, ptr, tiles, bf16)) return false;
+    g_maps.put(k, *m);
+    return true;
 }
 
 // sm_100 check, cached per device.
@@ -231,6 +300,24 @@ int dkdv_tail_units(int BH, int n_q) {
     return T < 0 ? 0 : (T > BH ? BH : T);
 }
 
+int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    return dev;
+}
+
+// One cudaFuncSetAttribute per (kernel instantiation, device): function attributes
+// are per-context state, so a process that drives several GPUs opts in on each.
+// Keyed on the kernel itself (different instantiations share a function-pointer type).
+template <auto kKernel>
+cudaError_t set_smem_once(int bytes) {
+    static std::once_flag once[64];
+    static cudaError_t err[64];
+    const int dev = current_device();
+    std::call_once(once[dev], [&] { err[dev] = cudaFuncSetAttribute(kKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
+    return err[dev];
+}
+
 // Launch with programmatic stream serialisation (see griddep_* in sm100_ptx.cuh):
 // the kernel's CTAs may start their prologue while the previous kernel drains.
 template <typename... Params, typename... Args>
@@ -254,7 +341,7 @@ cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, int sme
 
 template <int kD, bool kBF16, bool kDrop>
 int launch_forward(const vattn_config* c, const void* q, const void* k, const void* v, void* o,
-                   float* lse, uint32_t* drop_mask, cudaStream_t stream) {
+                   float* lse, uint32_t* drop_mask, unsigned int* status, cudaStream_t stream) {
     const int BH = units(c), N = c->seq_len;
     CUtensorMap mq, mk, mv, mo;
     if (!make_map(&mq, q, BH, N, kD, kBF16) || !make_map(&mk, k, BH, N, kD, kBF16) ||
@@ -262,11 +349,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
         return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled failed");
     auto kern = mha_fwd_sm100_kernel<kD, kBF16, kDrop>;
     constexpr int smem = FwdCfg<kD>::kSmemBytes;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    });
+    const cudaError_t attr_err = set_smem_once<mha_fwd_sm100_kernel<kD, kBF16, kDrop>>(smem);
     if (attr_err != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(attr_err));
     FwdParams p;
     p.lse = lse;
@@ -277,6 +360,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     set_dropout(c, &p.H, &p.bh_off, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
     p.drop_mask = drop_mask;
     p.mask_words = (N + 127) / 128 * 4;
+    p.status = status;
     const dim3 grid = tile_grid((N + 255) / 256, BH, c->causal ? bh_group(BH, 2ll * N * kD * 2, true) : 1);  // K, V
     {
         ProfScope prof(stream, 0);
@@ -319,6 +403,15 @@ size_t ds_cap_bytes() {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// VATTN_DROP_MASK=0: no keep-bit masks at all (both backward kernels hash in place).
+bool drop_mask_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("VATTN_DROP_MASK");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 BwdLayout bwd_layout(const vattn_config* c) {
     BwdLayout L{};
     const size_t BH = static_cast<size_t>(units(c));
@@ -345,10 +438,7 @@ BwdLayout bwd_layout(const vattn_config* c) {
     // hashed here once -- instead of hashing every position twice.  That also frees the
     // dK/dV kernel's row-hash buffer for the dS^T staging box, so dropout takes the dQ
     // GEMM path.  VATTN_DROP_MASK=0: hash in place (and recompute dQ).
-    static const bool mask_env = [] {
-        const char* e = getenv("VATTN_DROP_MASK");
-        return !(e && atoi(e) == 0);
-    }();
+    const bool mask_env = drop_mask_enabled();
     const size_t mask_bytes = BH * static_cast<size_t>(L.Npad) * (L.Npad / 8);
     L.drop_mask = c->dropout_p > 0.0f && mask_env;
     L.materialize_ds = c->dropout_p > 0.0f && !L.drop_mask
@@ -357,16 +447,6 @@ BwdLayout bwd_layout(const vattn_config* c) {
     L.mask = L.ds + (L.materialize_ds ? align256(ds_bytes) : 0);
     L.total = L.mask + (L.drop_mask ? align256(mask_bytes) : 0);
     return L;
-}
-
-// One cudaFuncSetAttribute per kernel instantiation (keyed on the kernel itself:
-// different instantiations share a function-pointer type).
-template <auto kKernel>
-cudaError_t set_smem_once(int bytes) {
-    static std::once_flag once;
-    static cudaError_t err = cudaSuccess;
-    std::call_once(once, [&] { err = cudaFuncSetAttribute(kKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
-    return err;
 }
 
 template <int kD, bool kBF16, bool kDrop>
@@ -496,6 +576,12 @@ int vattn_validate_(const vattn_config* cfg) { return validate(cfg); }
 
 int vattn_last_launch_count(void) { return g_launches; }
 
+void vattn_map_cache_stats(long long* hits, long long* misses) {
+    if (hits) *hits = g_map_hits.load();
+    if (misses) *misses = g_map_misses.load();
+}
+
+
 void vattn_profile_enable(int on) {
     std::lock_guard<std::mutex> l(g_prof_mu);
     for (auto& e : g_prof) {
@@ -524,7 +610,7 @@ int vattn_profile_read(int kind, double* ms_total, int* launches) {
 }
 
 static int forward_impl(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o, float* lse,
-                        uint32_t* mask, void* stream) {
+                        uint32_t* mask, unsigned int* status, void* stream) {
     g_launches = 0;
     int rc = validate(cfg);
     if (rc) return rc;
@@ -535,24 +621,46 @@ static int forward_impl(const vattn_config* cfg, const void* q, const void* k, c
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int sel = (cfg->head_dim == 128 ? 4 : 0) | (cfg->dtype == VATTN_BF16 ? 2 : 0) | (cfg->dropout_p > 0.0f ? 1 : 0);
     switch (sel) {
-        case 0: return launch_forward<64, false, false>(cfg, q, k, v, o, lse, mask, s);
-        case 1: return launch_forward<64, false, true>(cfg, q, k, v, o, lse, mask, s);
-        case 2: return launch_forward<64, true, false>(cfg, q, k, v, o, lse, mask, s);
-        case 3: return launch_forward<64, true, true>(cfg, q, k, v, o, lse, mask, s);
-        case 4: return launch_forward<128, false, false>(cfg, q, k, v, o, lse, mask, s);
-        case 5: return launch_forward<128, false, true>(cfg, q, k, v, o, lse, mask, s);
-        case 6: return launch_forward<128, true, false>(cfg, q, k, v, o, lse, mask, s);
-        default: return launch_forward<128, true, true>(cfg, q, k, v, o, lse, mask, s);
+        case 0: return launch_forward<64, false, false>(cfg, q, k, v, o, lse, mask, status, s);
+        case 1: return launch_forward<64, false, true>(cfg, q, k, v, o, lse, mask, status, s);
+        case 2: return launch_forward<64, true, false>(cfg, q, k, v, o, lse, mask, status, s);
+        case 3: return launch_forward<64, true, true>(cfg, q, k, v, o, lse, mask, status, s);
+        case 4: return launch_forward<128, false, false>(cfg, q, k, v, o, lse, mask, status, s);
+        case 5: return launch_forward<128, false, true>(cfg, q, k, v, o, lse, mask, status, s);
+        case 6: return launch_forward<128, true, false>(cfg, q, k, v, o, lse, mask, status, s);
+        default: return launch_forward<128, true, true>(cfg, q, k, v, o, lse, mask, status, s);
     }
 }
 
 int mha_forward(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o,
                 float* lse, void* stream) {
-    return forward_impl(cfg, q, k, v, o, lse, nullptr, stream);
+    return forward_impl(cfg, q, k, v, o, lse, nullptr, nullptr, stream);
+}
+
+// internal (capi_host.cu): forward of one slab with the domain-error word
+int vattn_forward_status_(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o, float* lse,
+                          unsigned int* status, void* stream) {
+    return forward_impl(cfg, q, k, v, o, lse, nullptr, status, stream);
+}
+
+int mha_forward_ex(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o, float* lse,
+                   void* drop_mask, unsigned int* status, void* stream) {
+    g_launches = 0;
+    int rc = validate(cfg);
+    if (rc) return rc;
+    if (drop_mask) {
+        if (cfg->dropout_p <= 0.0f) return fail(VATTN_EINVAL, "mha_forward_ex: drop_mask needs dropout_p > 0");
+        if (!drop_mask_enabled()) return fail(VATTN_EINVAL, "mha_forward_ex: keep-bit masks are disabled (VATTN_DROP_MASK=0)");
+        if ((reinterpret_cast<uintptr_t>(drop_mask) & 255u) != 0)
+            return fail(VATTN_EINVAL, "mha_forward_ex: mask must be 256-byte aligned");
+    }
+    if (status && (reinterpret_cast<uintptr_t>(status) & 3u) != 0)
+        return fail(VATTN_EINVAL, "mha_forward_ex: status word must be 4-byte aligned");
+    return forward_impl(cfg, q, k, v, o, lse, static_cast<uint32_t*>(drop_mask), status, stream);
 }
 
 size_t mha_dropout_mask_bytes(const vattn_config* cfg) {
-    if (validate(cfg) || cfg->dropout_p <= 0.0f) return 0;
+    if (validate(cfg) || cfg->dropout_p <= 0.0f || !drop_mask_enabled()) return 0;
     const size_t Npad = static_cast<size_t>((cfg->seq_len + 127) / 128) * 128;
     return static_cast<size_t>(units(cfg)) * Npad * (Npad / 8);
 }
@@ -565,7 +673,8 @@ int mha_forward_dropout_mask(const vattn_config* cfg, const void* q, const void*
     if (cfg->dropout_p <= 0.0f) return fail(VATTN_EINVAL, "mha_forward_dropout_mask: dropout_p must be > 0");
     if (!drop_mask || (reinterpret_cast<uintptr_t>(drop_mask) & 255u) != 0)
         return fail(VATTN_EINVAL, "mha_forward_dropout_mask: mask must be non-null and 256-byte aligned");
-    return forward_impl(cfg, q, k, v, o, lse, static_cast<uint32_t*>(drop_mask), stream);
+    if (!drop_mask_enabled()) return fail(VATTN_EINVAL, "mha_forward_dropout_mask: keep-bit masks are disabled (VATTN_DROP_MASK=0)");
+    return forward_impl(cfg, q, k, v, o, lse, static_cast<uint32_t*>(drop_mask), nullptr, stream);
 }
 
 int mha_dpsum(const vattn_config* cfg, const void* o, const void* dout, float* d_rows, void* stream) {
@@ -635,6 +744,12 @@ size_t mha_backward_workspace_bytes(const vattn_config* cfg) {
     return bwd_layout(cfg).total;
 }
 
+size_t mha_backward_workspace_bytes_mask(const vattn_config* cfg) {
+    if (validate(cfg)) return 0;
+    const BwdLayout L = bwd_layout(cfg);
+    return L.drop_mask ? L.mask : L.total;  // the caller's mask replaces the workspace's own
+}
+
 static int backward_impl(const vattn_config* cfg, const void* q, const void* k, const void* v, const void* o,
                          const void* dout, const float* lse, void* dq, void* dk, void* dv, void* workspace,
                          size_t workspace_bytes, const uint32_t* mask, void* stream) {
@@ -648,8 +763,12 @@ static int backward_impl(const vattn_config* cfg, const void* q, const void* k, 
         return fail(VATTN_EINVAL, "mha_backward: tensors must be 16-byte aligned");
     if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0)
         return fail(VATTN_EINVAL, "mha_backward: workspace must be 256-byte aligned");
-    if (workspace_bytes < bwd_layout(cfg).total)
-        return fail(VATTN_EINVAL, "mha_backward: workspace too small (see mha_backward_workspace_bytes)");
+    {
+        const BwdLayout L = bwd_layout(cfg);
+        // with the forward's keep bits (mask) the workspace needs no mask region of its own
+        if (workspace_bytes < ((mask && L.drop_mask) ? L.mask : L.total))
+            return fail(VATTN_EINVAL, "mha_backward: workspace too small (see mha_backward_workspace_bytes)");
+    }
     if ((rc = check_device())) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int sel = (cfg->head_dim == 128 ? 4 : 0) | (cfg->dtype == VATTN_BF16 ? 2 : 0) | (cfg->dropout_p > 0.0f ? 1 : 0);
@@ -678,7 +797,7 @@ int mha_backward(const vattn_config* cfg, const void* q, const void* k, const vo
 // backward reads them (no second hash pass).
 int vattn_step_device_(const vattn_config* cfg, const void* q, const void* k, const void* v, const void* dout, void* o,
                        float* lse, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
-                       void* stream) {
+                       unsigned int* status, void* stream) {
     int rc = validate(cfg);
     if (rc) return rc;
     uint32_t* mask = nullptr;
@@ -687,7 +806,7 @@ int vattn_step_device_(const vattn_config* cfg, const void* q, const void* k, co
         if (L.drop_mask && workspace && workspace_bytes >= L.total)
             mask = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) + L.mask);
     }
-    rc = forward_impl(cfg, q, k, v, o, lse, mask, stream);
+    rc = forward_impl(cfg, q, k, v, o, lse, mask, status, stream);
     if (rc) return rc;
     return backward_impl(cfg, q, k, v, o, dout, lse, dq, dk, dv, workspace, workspace_bytes, mask, stream);
 }

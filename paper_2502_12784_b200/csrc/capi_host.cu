@@ -97,9 +97,11 @@ struct Job {
     HostT out[kMaxT];
     int n_out = 0;
     size_t ws_unit = 0;  // device scratch bytes per unit (backward workspace)
-    // run the kernels of one slab: d_in[i] / d_out[i] point at the slot's buffers
+    // run the kernels of one slab: d_in[i] / d_out[i] point at the slot's buffers;
+    // `status` is the call's device domain-error word (the forward ORs into it)
     int (*run)(const vattn_config* slab, void* const* d_in, void* const* d_out, void* ws, size_t ws_bytes,
-               cudaStream_t s) = nullptr;
+               unsigned int* status, cudaStream_t s) = nullptr;
+    bool check_domain = false;  // map a non-zero status word to VATTN_EDOMAIN
 };
 
 int units_of(const vattn_config* c) { return c->bh_count ? c->bh_count : c->batch * c->heads; }
@@ -134,14 +136,26 @@ int run_pipeline(const vattn_config* cfg, const Job& job, cudaStream_t stream) {
     size_t slot_bytes = 0;
     for (int i = 0; i < job.n_in; ++i) slot_bytes += al(job.in[i].unit * cu_units);
     for (int i = 0; i < job.n_out; ++i) slot_bytes += al(job.out[i].unit * cu_units);
-    vattn_config full_slab = *cfg;
-    full_slab.bh_offset = cfg->bh_offset;
-    full_slab.bh_count = cu_units;
-    const size_t ws_bytes = job.ws_unit ? mha_backward_workspace_bytes(&full_slab) : 0;
+    // workspace: the largest over the full and the (smaller) last slab -- the backward's
+    // dQ design is chosen from a slab's own unit count, so a short last slab may need
+    // more than a full one (e.g. it falls under the dS materialisation cap)
+    size_t ws_bytes = 0;
+    if (job.ws_unit) {
+        vattn_config sl = *cfg;
+        sl.bh_count = cu_units;
+        ws_bytes = mha_backward_workspace_bytes(&sl);
+        const int last = U - (n_slabs - 1) * cu_units;
+        if (last != cu_units) {
+            sl.bh_count = last;
+            ws_bytes = std::max(ws_bytes, mha_backward_workspace_bytes(&sl));
+        }
+    }
     slot_bytes += al(ws_bytes);
 
     uint8_t* base = nullptr;
-    cu(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&base), slot_bytes * R, pool, stream), "staging alloc");
+    cu(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&base), slot_bytes * R + 256, pool, stream), "staging alloc");
+    unsigned int* status = reinterpret_cast<unsigned int*>(base + slot_bytes * R);
+    unsigned int h_status = 0;
     cudaEvent_t ready, in_done[3], comp_done[3], out_done[3];
     cu(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
     for (int r = 0; r < 3; ++r) {
@@ -152,6 +166,7 @@ int run_pipeline(const vattn_config* cfg, const Job& job, cudaStream_t stream) {
     int rc = VATTN_OK;
     try {
         // the staging buffers (and everything the caller queued) precede the copies
+        cu(cudaMemsetAsync(status, 0, sizeof(unsigned int), stream), "status memset");
         cu(cudaEventRecord(ready, stream), "event record");
         cu(cudaStreamWaitEvent(cs.in, ready, 0), "wait");
         cu(cudaStreamWaitEvent(cs.out, ready, 0), "wait");
@@ -183,7 +198,7 @@ int run_pipeline(const vattn_config* cfg, const Job& job, cudaStream_t stream) {
             vattn_config slab = *cfg;
             slab.bh_offset = cfg->bh_offset + u0;
             slab.bh_count = nu;
-            chk(job.run(&slab, d_in, d_out, ws, ws_bytes, stream), "slab kernels");
+            chk(job.run(&slab, d_in, d_out, ws, ws_bytes, status, stream), "slab kernels");
             cu(cudaEventRecord(comp_done[r], stream), "event record");
             // D2H
             cu(cudaStreamWaitEvent(cs.out, comp_done[r], 0), "wait");
@@ -195,6 +210,8 @@ int run_pipeline(const vattn_config* cfg, const Job& job, cudaStream_t stream) {
         }
         // join: the caller's stream owns the staging memory again, then release it
         cu(cudaStreamWaitEvent(stream, out_done[(n_slabs - 1) % R], 0), "wait");
+        if (job.check_domain)
+            cu(cudaMemcpyAsync(&h_status, status, sizeof(unsigned int), cudaMemcpyDeviceToHost, stream), "status D2H");
     } catch (const Fail& f) {
         rc = f.code;
         cudaStreamSynchronize(cs.in);
@@ -212,6 +229,11 @@ int run_pipeline(const vattn_config* cfg, const Job& job, cudaStream_t stream) {
         g_host_err = std::string("host pipeline: ") + cudaGetErrorString(se);
         rc = VATTN_ECUDA;
     }
+    if (rc == VATTN_OK && h_status != 0) {
+        // the reference throws std::domain_error here (online_softmax.cpp:33-34, 81-82)
+        g_host_err = "softmax: NaN score or fully masked row (l == 0) in a query row (domain error)";
+        rc = VATTN_EDOMAIN;
+    }
     return rc;
 }
 
@@ -222,7 +244,10 @@ size_t lse_unit(const vattn_config* c) { return static_cast<size_t>(c->seq_len) 
 extern "C" int vattn_validate_(const vattn_config* cfg);  // capi.cu
 extern "C" int vattn_step_device_(const vattn_config* cfg, const void* q, const void* k, const void* v,
                                   const void* dout, void* o, float* lse, void* dq, void* dk, void* dv,
-                                  void* workspace, size_t workspace_bytes, void* stream);  // capi.cu
+                                  void* workspace, size_t workspace_bytes, unsigned int* status,
+                                  void* stream);  // capi.cu
+extern "C" int vattn_forward_status_(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o,
+                                     float* lse, unsigned int* status, void* stream);  // capi.cu
 namespace {
 
 // The device entry points' own validation (same codes and messages).
@@ -232,18 +257,21 @@ int precheck(const vattn_config* c) {
     return rc;
 }
 
-int run_fwd(const vattn_config* s, void* const* in, void* const* out, void*, size_t, cudaStream_t st) {
-    return mha_forward(s, in[0], in[1], in[2], out[0], static_cast<float*>(out[1]), st);
+int run_fwd(const vattn_config* s, void* const* in, void* const* out, void*, size_t, unsigned int* status,
+            cudaStream_t st) {
+    return vattn_forward_status_(s, in[0], in[1], in[2], out[0], static_cast<float*>(out[1]), status, st);
 }
 
-int run_bwd(const vattn_config* s, void* const* in, void* const* out, void* ws, size_t wsb, cudaStream_t st) {
+int run_bwd(const vattn_config* s, void* const* in, void* const* out, void* ws, size_t wsb, unsigned int*,
+            cudaStream_t st) {
     return mha_backward(s, in[0], in[1], in[2], in[3], in[4], static_cast<const float*>(in[5]), out[0], out[1],
                         out[2], ws, wsb, st);
 }
 
-int run_step(const vattn_config* s, void* const* in, void* const* out, void* ws, size_t wsb, cudaStream_t st) {
+int run_step(const vattn_config* s, void* const* in, void* const* out, void* ws, size_t wsb, unsigned int* status,
+             cudaStream_t st) {
     return vattn_step_device_(s, in[0], in[1], in[2], in[3], out[0], static_cast<float*>(out[1]), out[2], out[3],
-                              out[4], ws, wsb, st);
+                              out[4], ws, wsb, status, st);
 }
 
 template <typename F>
@@ -281,6 +309,7 @@ int mha_forward_host(const vattn_config* cfg, const void* q, const void* k, cons
         j.out[1] = {nullptr, reinterpret_cast<uint8_t*>(lse), lse_unit(cfg)};
         j.n_out = 2;
         j.run = run_fwd;
+        j.check_domain = true;
         rc = guarded([&] { return run_pipeline(cfg, j, static_cast<cudaStream_t>(stream)); });
     }
     if (rc) vattn_set_error_(g_host_err.c_str());
@@ -339,6 +368,7 @@ int mha_step_host(const vattn_config* cfg, const void* q, const void* k, const v
         j.n_out = 5;
         j.ws_unit = 1;
         j.run = run_step;
+        j.check_domain = true;
         rc = guarded([&] { return run_pipeline(cfg, j, static_cast<cudaStream_t>(stream)); });
     }
     if (rc) vattn_set_error_(g_host_err.c_str());

@@ -160,7 +160,7 @@ struct DkdvCfg {
     // bits are hashed in place (no keep-bit mask) -- and then materialisation is off.
     static constexpr int kSmemDsStage = kSmemDrop;
     static constexpr int kSmemBar = kSmemDsStage + 32768;
-    static constexpr int kNumBars = 16;
+    static constexpr int kNumBars = 20;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr uint32_t kTmemS = 0;                       // region r at 128 r
     static constexpr uint32_t kTmemDP = kDoubleS ? 256 : 128;
@@ -195,8 +195,15 @@ __global__ void __launch_bounds__(384, 1)
     constexpr bool kDB = Cfg::kDoubleS;
     uint64_t* s_full = q_empty + kSt;     // [kDB ? 2 : 1] per S region
     uint64_t* dp_full = s_full + (kDB ? 2 : 1);
-    uint64_t* p_full = dp_full + 1;   // [warpgroup]
-    uint64_t* ds_full = p_full + 2;   // [warpgroup]
+    // p_full[s & 1][warpgroup]: one barrier per step parity.  With the double S region
+    // (d = 64) a warpgroup may publish P^T_(s+1) before the MMA warp consumed its P^T_s
+    // phase (S_(s+1) is issued a step early); on a single barrier that second phase
+    // aliases the first under parity waits (the MMA then waits for phase s + 2 -> hang)
+    // and the early arrival can complete phase s before a slow warp of the same
+    // warpgroup wrote its rows (race).  Two barriers keep every phase distinct: a
+    // warpgroup can never run two steps ahead (dP_(s+1) needs dK_s, i.e. all of dS_s).
+    uint64_t* p_full = dp_full + 1;   // [2][warpgroup]
+    uint64_t* ds_full = p_full + 4;   // [warpgroup]
     uint64_t* dkv_full = ds_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
@@ -219,10 +226,8 @@ __global__ void __launch_bounds__(384, 1)
         mbar_init(s_full, 1);
         if (kDB) mbar_init(s_full + 1, 1);
         mbar_init(dp_full, 1);
-        for (int x = 0; x < 2; ++x) {
-            mbar_init(p_full + x, 4);  // one arrive per warp of warpgroup x
-            mbar_init(ds_full + x, 4);
-        }
+        for (int x = 0; x < 4; ++x) mbar_init(p_full + x, 4);  // one arrive per warp of warpgroup x & 1
+        for (int x = 0; x < 2; ++x) mbar_init(ds_full + x, 4);
         mbar_init(dkv_full, 1);
         fence_barrier_init();
     }
@@ -249,6 +254,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int s = 0; s < n_steps; ++s) {
                 const int st = s % kSt;
                 const int i = i0 + s;
+                stress_delay(4, s);
                 mbar_wait(q_empty + st, ((s / kSt) & 1) ^ 1);
                 mbar_arrive_expect_tx(q_full + st, 2 * Cfg::kTileBytes + 1024);
                 for (int b = 0; b < Cfg::kBoxes; ++b) {
@@ -309,7 +315,8 @@ __global__ void __launch_bounds__(384, 1)
             for (int s = 0; s < n_steps; ++s) {
                 const int st = s % kSt, st1 = (s + 1) % kSt, st2 = (s + 2) % kSt;
                 const uint32_t R = (s & 1) * 128u;
-                issue_ts(Cfg::kTmemDV, Cfg::kTmemS + R, dDOm + st * kTile16, s > 0, p_full, s & 1);  // dV += P^T dO
+                stress_delay(3, s);
+                issue_ts(Cfg::kTmemDV, Cfg::kTmemS + R, dDOm + st * kTile16, s > 0, p_full + 2 * (s & 1), (s >> 1) & 1);  // dV += P^T dO
                 issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, s & 1);      // dK += dS^T Q
                 mma_commit_e(q_empty + st);
                 if (s + 1 < n_steps) {
@@ -327,7 +334,8 @@ __global__ void __launch_bounds__(384, 1)
         for (int s = 0; s < n_steps; ++s) {
             const int st = s % kSt;
             const int st1 = (s + 1) % kSt;
-            issue_ts(Cfg::kTmemDV, Cfg::kTmemS, dDOm + st * kTile16, s > 0, p_full, s & 1);  // dV += P^T dO
+            stress_delay(3, s);
+            issue_ts(Cfg::kTmemDV, Cfg::kTmemS, dDOm + st * kTile16, s > 0, p_full + 2 * (s & 1), (s >> 1) & 1);  // dV += P^T dO
             VTRACE(8 * s + 0);
             if (s + 1 < n_steps) {
                 mbar_wait(q_full + st1, ((s + 1) / kSt) & 1);
@@ -365,6 +373,7 @@ __global__ void __launch_bounds__(384, 1)
             mbar_wait(q_full + st, (s / kSt) & 1);  // lse2 / D of this tile landed
             mbar_wait(s_full + (kDB ? (s & 1) : 0), kDB ? ((s >> 1) & 1) : (s & 1));
             tc_fence_after();
+            stress_delay(1, s);
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 0);
             float pr[64];
             tmem_ld32f(tmem + lb + sR + 64 * h, pr);
@@ -449,8 +458,9 @@ __global__ void __launch_bounds__(384, 1)
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(p_full + h);
+            if (lane == 0) mbar_arrive(p_full + 2 * (s & 1) + h);
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 1);
+            stress_delay(2, s);
 
             mbar_wait(dp_full, s & 1);
             tc_fence_after();
@@ -573,7 +583,7 @@ struct DqCfg {
     static constexpr int kSmemK = 2 * kTileBytes;
     static constexpr int kSmemV = kSmemK + kKSlots * kTileBytes;
     static constexpr int kSmemBar = kSmemV + kVSlots * kTileBytes;
-    static constexpr int kNumBars = 1 + 2 * kKSlots + 2 * kVSlots + 2 + 1 + 1 + 1 + 1;
+    static constexpr int kNumBars = 1 + 2 * kKSlots + 2 * kVSlots + 2 + 1 + 2 + 1 + 1;
     // d = 64: dP_(j+1) is issued as soon as the math warps hold dP_j in registers
     // (measured -4..5 % on the dQ kernel at d = 64; at d = 128 it delays S_(j+2) and loses)
     static constexpr bool kEarlyDP = kD == 64;
@@ -606,8 +616,13 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* v_empty = v_full + SV;        // [SV]
     uint64_t* s_full = v_empty + SV;        // [2] per S region
     uint64_t* dp_full = s_full + 2;
-    uint64_t* ds_full = dp_full + 1;
-    uint64_t* dq_done = ds_full + 1;
+    // ds_full[j & 1] (8 arrivals each).  With the early dP (d = 64) a fast warp can
+    // finish dS_(j+1) before a slow warp arrived for dS_j (dP_(j+1) only needs every
+    // warp to have LOADED dP_j); on one barrier its arrival would complete phase j
+    // early (the MMA would read the slow warp's dS_j half written).  Two barriers
+    // separate the phases; no warp can reach dS_(j+2) before all finished dS_j.
+    uint64_t* ds_full = dp_full + 1;        // [2]
+    uint64_t* dq_done = ds_full + 2;
     uint64_t* dp_empty = dq_done + 1;       // kEarlyDP: all 8 math warps loaded dP_j
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
@@ -633,7 +648,8 @@ __global__ void __launch_bounds__(384, 1)
         mbar_init(s_full + 0, 1);
         mbar_init(s_full + 1, 1);
         mbar_init(dp_full, 1);
-        mbar_init(ds_full, 8);
+        mbar_init(ds_full + 0, 8);
+        mbar_init(ds_full + 1, 8);
         mbar_init(dq_done, 1);
         mbar_init(dp_empty, 8);
         fence_barrier_init();
@@ -677,6 +693,7 @@ __global__ void __launch_bounds__(384, 1)
             load_k(0);
             if (nk > 1) load_k(1);
             for (int j = 0; j < nk; ++j) {
+                stress_delay(4, j);
                 load_v(j);
                 if (j + 2 < nk) load_k(j + 2);
             }
@@ -731,7 +748,8 @@ __global__ void __launch_bounds__(384, 1)
                     mma_commit_e(v_empty + (j + 1) % SV);
                 }
             }
-            mbar_wait_mma(ds_full, j & 1);
+            stress_delay(3, j);
+            mbar_wait_mma(ds_full + (j & 1), (j >> 1) & 1);
             tc_fence_after();
             VTRACE(8 * j + 0);
             // dQ += dS K_j : A = dS in TMEM (warpgroup h: keys [64h, 64h+64) at R + 64h + [0,32))
@@ -776,6 +794,7 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t R = (j & 1) ? 128u : 0u;
             mbar_wait<VATTN_SLEEP_MATH, true>(s_full + (j & 1), (j >> 1) & 1);
             tc_fence_after();
+            stress_delay(1, j);
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 0);
             float pr[64];
             tmem_ld32f(tmem + lb + R + 64 * h, pr);
@@ -811,6 +830,7 @@ __global__ void __launch_bounds__(384, 1)
                     if (x > lim) pr[x] = 0.0f;
             }
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 1);
+            stress_delay(2, j);
             mbar_wait<VATTN_SLEEP_MATH, true>(dp_full, j & 1);
             tc_fence_after();
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 2);
@@ -860,7 +880,7 @@ __global__ void __launch_bounds__(384, 1)
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(ds_full);
+            if (lane == 0) mbar_arrive(ds_full + (j & 1));
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * j + 3);
         }
         // ------------------------------------- epilogue: dQ * scale -> 16-bit
@@ -964,6 +984,7 @@ __global__ void __launch_bounds__(256, 1)
             const long long tile0 = static_cast<long long>(bh) * p.ds_tiles_per_bh + ds_tile_index(p, i, 0);
             for (int j = 0; j < nk; ++j) {
                 const int st = j % S;
+                stress_delay(4, j);
                 mbar_wait<VATTN_SLEEP_PRODUCER>(empty + st, ((j / S) & 1) ^ 1);
                 mbar_arrive_expect_tx(full + st, Cfg::kStageBytes);
                 uint8_t* ds = smem + st * Cfg::kStageBytes;
@@ -981,6 +1002,7 @@ __global__ void __launch_bounds__(256, 1)
         constexpr uint64_t kStage16 = Cfg::kStageBytes >> 4;
         for (int j = 0; j < nk; ++j) {
             const int st = j % S;
+            stress_delay(3, j);
             mbar_wait_mma(full + st, (j / S) & 1);
             tc_fence_after();
 #pragma unroll

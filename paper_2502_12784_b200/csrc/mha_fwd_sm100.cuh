@@ -41,6 +41,10 @@ struct FwdParams {
     // the backward (mha_forward_dropout_mask); nullptr = not kept
     uint32_t* drop_mask;
     int mask_words;        // Npad / 32
+    // optional device word: bit VATTN_DOMAIN_ROW (1) is OR-ed in when a query row had a
+    // NaN / +inf score or an empty softmax sum (l == 0), the reference's domain_error
+    // cases (online_softmax.cpp:33-34, 81-82); nullptr = unchecked
+    unsigned int* status;
 };
 
 template <int kD>
@@ -139,6 +143,7 @@ __global__ void __launch_bounds__(384, 1)
                                 q0 + 128 * t, bh);
             }
             for (int j = 0; j < nkmax; ++j) {
+                stress_delay(4, j);
 #pragma unroll
                 for (int w = 0; w < 2; ++w) {
                     const int pos = 2 * j + w;
@@ -202,6 +207,7 @@ __global__ void __launch_bounds__(384, 1)
             mma_commit_e(kv_empty + 0);
         }
         for (int j = 0; j < nkmax; ++j) {
+            stress_delay(3, j);
             wait_kv(2 * j + 1);
             bool k_next = false;
 #pragma unroll
@@ -236,10 +242,12 @@ __global__ void __launch_bounds__(384, 1)
         if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H), row);
         float m_run = -INFINITY;  // running max, log2 units (already scaled)
         float l_run = 0.0f;
+        bool bad = false;         // a NaN or +inf score in this row (FMNMX.NAN keeps NaN in mx)
         const int ntile = t ? nk[1] : nk[0];
         for (int j = 0; j < ntile; ++j) {
             mbar_wait<VATTN_SLEEP_MATH>(s_full + t, j & 1);
             tc_fence_after();
+            stress_delay(1, j);
             if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 0);
             float s[128];
             tmem_ld32f(tS + 0, s);
@@ -260,6 +268,7 @@ __global__ void __launch_bounds__(384, 1)
             }
             // row max: tree of 3-input maxima
             const float mx = row_max<128>(s);
+            bad |= !(mx < INFINITY);
             const float m_tile = mx * sc;
             if ((warp & 3) == 0 && lane == 0) VTRACE(2048 + 8 * j + 4 * t + 1);
             if (j == 0) {
@@ -373,6 +382,7 @@ __global__ void __launch_bounds__(384, 1)
             if (row < N) {
                 const float m_use = m_run == -INFINITY ? 0.0f : m_run;
                 p.lse[static_cast<size_t>(bh) * N + row] = (m_use + lg2(l_run)) * 0.69314718055994530942f;
+                if (p.status && (bad || !(l_run > 0.0f))) atomicOr(p.status, 1u);
             }
             uint8_t* sO = sQ + t * Cfg::kTileBytes;  // Q_t is dead once the last S_t landed
 #pragma unroll

@@ -205,6 +205,40 @@ VATTN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Schedule fuzzer (stress builds only, -DVATTN_STRESS_NS=<ns>; compiled out by
+// default): parks the calling warp for a pseudo-random 0..VATTN_STRESS_NS ns at
+// one in eight of the points it is called from, so warps and warpgroups drift
+// apart by whole pipeline steps.  The value depends only on warp-uniform inputs
+// (block, warp, call site, step), so every active lane takes the same branch (the
+// producer calls it from its single elected lane).  tests/test_stress_gpu.py soaks every kernel
+// under it: a barrier protocol that relies on warps staying in lock step hangs
+// (watchdog trap) or races there.
+#ifndef VATTN_STRESS_NS
+#define VATTN_STRESS_NS 0
+#endif
+VATTN_DEV void stress_delay(uint32_t site, uint32_t step) {
+#if VATTN_STRESS_NS
+    uint32_t x = blockIdx.x * 0x9E3779B1u ^ blockIdx.y * 0x85EBCA77u ^ (threadIdx.x >> 5) * 0xC2B2AE3Du ^
+                 site * 0x27D4EB2Fu ^ step * 0x165667B1u;
+    x ^= x >> 15;
+    x *= 0x2C1B3C6Du;
+    x ^= x >> 12;
+    x *= 0x297A2D39u;
+    x ^= x >> 15;
+    if ((x & 7u) == 0) {
+        uint32_t ns = (x >> 8) % static_cast<uint32_t>(VATTN_STRESS_NS);
+        while (ns > 0) {
+            const uint32_t chunk = ns > 100000u ? 100000u : ns;
+            __nanosleep(chunk);
+            ns -= chunk;
+        }
+    }
+#else
+    (void)site;
+    (void)step;
+#endif
+}
+
 // Role-specific wait policy (bit set = that role parks instead of spinning).
 #ifndef VATTN_SLEEP_MASK
 #define VATTN_SLEEP_MASK 1
@@ -593,22 +627,25 @@ VATTN_DEV float ex2_mix(int pair, float x) {
     return ex2(x);
 }
 
-// fmax the compiler cannot re-associate into one dependent FMNMX3 chain
+// fmax the compiler cannot re-associate into one dependent FMNMX3 chain.  The .NaN
+// flavour (FMNMX.NAN) propagates a NaN operand instead of dropping it, so a NaN
+// score reaches the row maximum (the forward's domain-error flag, like the
+// reference's NaN-score check, online_softmax.cpp:33-34).
 VATTN_DEV float fmax_nr(float a, float b) {
     float r;
-    asm("max.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
     return r;
 }
 
-// 3-input max (FMNMX3): halves the instructions of a row-max tree.
+// 3-input max (FMNMX3.NAN): halves the instructions of a row-max tree.
 VATTN_DEV float fmax3(float a, float b, float c) {
     float r;
-    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
     return r;
 }
 
 // Max of an unrolled register array: 8 independent chains of 3-input maxima
-// (few live temporaries, depth kN/16 + 3).
+// (few live temporaries, depth kN/16 + 3); NaN if any element is NaN.
 template <int kN>
 VATTN_DEV float row_max(const float* v) {
     static_assert(kN % 16 == 0 && kN >= 16, "row_max");

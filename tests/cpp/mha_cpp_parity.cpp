@@ -122,6 +122,37 @@ int main() {
         catch (const std::invalid_argument&) { threw = true; }
         check(threw, "shape mismatch throws std::invalid_argument");
     }
+    // numerical-domain errors mirror the reference (std::domain_error): a NaN in one Q
+    // row makes the reference's forward_fused (online_softmax.cpp:33-34) and its
+    // backward_fused (which re-runs the forward) throw; so must the B200 API, on the
+    // native-d host pipeline (mha_forward_host) and on the padded-d path (mha_forward_ex)
+    for (int d : {64, 20}) {
+        const std::vector<size_t> dims{1, 2, 128, (size_t)d};
+        auto q = vattn::normal_tensor_f16(5, 1, dims);
+        const auto k = vattn::normal_tensor_f16(5, 2, dims), v = vattn::normal_tensor_f16(5, 3, dims),
+                   dout = vattn::normal_tensor_f16(5, 4, dims);
+        q.data()[(128 + 77) * d + 3] = vattn::Half::from_bits(0x7e00);  // NaN in head 1, row 77
+        vattn::AttnConfig rc;
+        rc.heads = 2; rc.seq_len = 128; rc.head_dim = d;
+        vattn_b200::AttnConfig bc;
+        bc.heads = 2; bc.seq_len = 128; bc.head_dim = d;
+        auto throws_domain = [](auto&& f) {
+            try { f(); } catch (const std::domain_error&) { return true; } catch (...) { return false; }
+            return false;
+        };
+        const std::string tag = "d" + std::to_string(d) + ": ";
+        check(throws_domain([&] { vattn::forward_fused(q, k, v, rc); }),
+              tag + "reference forward_fused throws std::domain_error on a NaN score");
+        check(throws_domain([&] { vattn_b200::forward_fused(bits(q), bits(k), bits(v), bc); }),
+              tag + "vattn_b200::forward_fused throws std::domain_error on a NaN score");
+        const std::vector<float> lse(2 * 128, 0.0f);
+        check(throws_domain([&] { vattn_b200::backward_fused(bits(q), bits(k), bits(v), bits(dout), lse, bc); }),
+              tag + "vattn_b200::backward_fused (re-runs the forward) throws std::domain_error");
+        // the same call on finite inputs does not throw (the flag is per call)
+        const auto q_ok = vattn::normal_tensor_f16(5, 1, dims);
+        check(!throws_domain([&] { vattn_b200::forward_fused(bits(q_ok), bits(k), bits(v), bc); }),
+              tag + "finite inputs after a domain error: no throw");
+    }
     std::printf("%d failure(s)\n", g_fail);
     return g_fail;
 }

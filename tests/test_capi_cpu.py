@@ -121,4 +121,4 @@ def test_python_mirror_config_validation():
         vb.AttnConfig(seq_len=64, head_dim=64, dropout_p=1.0).validate()
     vb.AttnConfig(seq_len=100, head_dim=64).validate(strict_tiles=False)
     assert abs(vb.AttnConfig(seq_len=64, head_dim=64).scale() - 0.125) < 1e-9
-    assert vb.lib.vattn_abi_version() == 3
+    assert vb.lib.vattn_abi_version() == 4
