@@ -60,7 +60,12 @@ CONFIGS = {
     "c3_nc": (4, 16, 8192, 128, False, "bf16", "BASELINE configs[2] shape, non-causal: d=128, B=4, H=16, N=8192, bf16"),
     "c4": (8, 16, 1024, 64, True, "fp16", "BASELINE configs[3] per layer: GPT-2-medium attention, causal"),
     "c5": (1, 64, 32768, 128, True, "bf16", "BASELINE configs[4] on one GPU: causal seq 32k, d=128, H=64"),
+    "c4x24": (8, 16, 1024, 64, True, "fp16", "BASELINE configs[3]: GPT-2-medium attention training step, "
+              "24 layers (24 forwards, then 24 backwards in reverse) captured as one CUDA graph, causal"),
+    "c1": (1, 2, 128, 64, False, "fp16", "BASELINE configs[0]: the CPU oracle shape (launch-bound)"),
 }
+# configs whose step runs several attention layers (distinct tensors per layer)
+LAYERS = {"c4x24": 24}
 
 
 def flops(B, H, N, d, causal):
@@ -316,23 +321,52 @@ def main():
         # this rank's (b, h) slab of the global [B*world, H] problem (dropout masks use global (b, h))
         slab = (B * world, H, rank * B * H, B * H) if world > 1 else None
         units_total = B * H * world
-    o = torch.empty(shape, device=dev, dtype=dtype)
-    lse = torch.empty(shape[:3], device=dev, dtype=torch.float32)
-    dq, dk, dv = (torch.empty(shape, device=dev, dtype=dtype) for _ in range(3))
+    layers = LAYERS.get(args.config, 1)
+    if layers > 1 and strong:
+        raise SystemExit("--split bh is for single-layer configs")
     n_units_rank = shape[0] * shape[1]
-    ws = torch.empty(vb.workspace_bytes(n_units_rank, 1, N, d, causal, dtype, args.dropout), dtype=torch.uint8,
-                     device=dev)
     stream = torch.cuda.current_stream()
 
-    # dropout: the forward keeps its keep bits for the backward (as the autograd binding does)
-    mask = (torch.empty(vb.dropout_mask_bytes(q, causal, args.dropout, slab), dtype=torch.uint8, device=dev)
-            if args.dropout > 0 else None)
+    def buffers(q, k, v, do):
+        return dict(q=q, k=k, v=v, do=do, o=torch.empty(shape, device=dev, dtype=dtype),
+                    lse=torch.empty(shape[:3], device=dev, dtype=torch.float32),
+                    dq=torch.empty(shape, device=dev, dtype=dtype), dk=torch.empty(shape, device=dev, dtype=dtype),
+                    dv=torch.empty(shape, device=dev, dtype=dtype),
+                    # dropout: the forward keeps its keep bits for the backward (as the autograd binding does)
+                    mask=(torch.empty(vb.dropout_mask_bytes(q, causal, args.dropout, slab), dtype=torch.uint8,
+                                      device=dev) if args.dropout > 0 else None))
 
-    def step():
-        vb.mha_forward(q, k, v, causal, out=o, lse=lse, dropout_p=args.dropout, seed=1234, bh_slab=slab,
-                       drop_mask=mask)
-        vb.mha_backward(q, k, v, o, do, lse, causal, dq=dq, dk=dk, dv=dv, workspace=ws,
-                        dropout_p=args.dropout, seed=1234, bh_slab=slab, drop_mask=mask)
+    Ls = [buffers(q, k, v, do)]
+    for _ in range(layers - 1):  # further layers: their own inputs (same shapes)
+        Ls.append(buffers(*(torch.randn(shape, generator=gen, device=dev, dtype=torch.float32).to(dtype)
+                            for _ in range(4))))
+    mask = Ls[0]["mask"]
+    ws = torch.empty(vb.workspace_bytes(n_units_rank, 1, N, d, causal, dtype, args.dropout,
+                                        external_mask=mask is not None), dtype=torch.uint8, device=dev)
+    o, lse, dq, dk, dv = (Ls[0][x] for x in ("o", "lse", "dq", "dk", "dv"))
+
+    def step_eager():
+        for x in Ls:  # forwards through the layers
+            vb.mha_forward(x["q"], x["k"], x["v"], causal, out=x["o"], lse=x["lse"], dropout_p=args.dropout,
+                           seed=1234, bh_slab=slab, drop_mask=x["mask"])
+        for x in reversed(Ls):  # backwards in reverse layer order
+            vb.mha_backward(x["q"], x["k"], x["v"], x["o"], x["do"], x["lse"], causal, dq=x["dq"], dk=x["dk"],
+                            dv=x["dv"], workspace=ws, dropout_p=args.dropout, seed=1234, bh_slab=slab,
+                            drop_mask=x["mask"])
+
+    step = step_eager
+    if layers > 1:
+        # one CUDA graph per training step (C4 "capture as a CUDA Graph")
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(cap):
+            step_eager()  # smem opt-ins and tensor maps outside the capture
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=cap):
+                step_eager()
+        stream.wait_stream(cap)
+        step = graph.replay
 
     for _ in range(args.warmup):
         step()
@@ -341,7 +375,7 @@ def main():
     # ---------------------------------------------------------------- timed
     # (no per-kernel events inside the timed region: an event between two kernels
     # would break their programmatic-dependent-launch overlap)
-    launches_per_step = 4  # fwd + (preprocess, dK/dV kernel, dQ kernel or dQ GEMM)
+    launches_per_step = 4 * layers  # per layer: fwd + (preprocess, dK/dV kernel, dQ kernel or dQ GEMM)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -363,7 +397,7 @@ def main():
     import ctypes as C
     vb.lib.vattn_profile_enable(1)
     for _ in range(max(3, min(args.steps, 10))):
-        step()
+        step_eager()
     torch.cuda.synchronize()
     kern_ms = []
     for kind in (0, 1, 2, 3):  # VATTN_KERNEL_FWD, _BWD_DKDV, _BWD_DQ, _BWD_PRE
@@ -377,8 +411,8 @@ def main():
     ms_max, fwd_ms, dkdv_ms, dq_ms, pre_ms = t.tolist()
     ms_step = ms_max / args.steps
     f_unit_fwd, f_unit_bwd = flops(1, 1, N, d, causal)
-    f_fwd, f_bwd = n_units_rank * f_unit_fwd, n_units_rank * f_unit_bwd  # this rank's (= max rank's) work
-    value = units_total * (f_unit_fwd + f_unit_bwd) / (ms_step * 1e-3) / 1e12
+    f_fwd, f_bwd = n_units_rank * f_unit_fwd, n_units_rank * f_unit_bwd  # one layer of this rank's work
+    value = layers * units_total * (f_unit_fwd + f_unit_bwd) / (ms_step * 1e-3) / 1e12
 
     # --------------------------------------------------- gather + verify (bh)
     verify = None
@@ -398,8 +432,9 @@ def main():
     d2h = sum(x.numel() * x.element_size() for x in (ho, hlse, hdq, hdk, hdv))
 
     def e2e_step():
-        vb.mha_step_host(hq, hk, hv, hdo, causal, dropout_p=args.dropout, seed=1234,
-                         out=(ho, hlse, hdq, hdk, hdv), bh_slab=slab)
+        for _ in range(layers):  # (every layer's tensors have the same size; layer 0's buffers stand in)
+            vb.mha_step_host(hq, hk, hv, hdo, causal, dropout_p=args.dropout, seed=1234,
+                             out=(ho, hlse, hdq, hdk, hdv), bh_slab=slab)
 
     e2e_ms = e2e_val = None
     if args.e2e_steps > 0:
@@ -417,7 +452,7 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = te.item() / args.e2e_steps
-        e2e_val = units_total * (f_unit_fwd + f_unit_bwd) / (e2e_ms * 1e-3) / 1e12
+        e2e_val = layers * units_total * (f_unit_fwd + f_unit_bwd) / (e2e_ms * 1e-3) / 1e12
 
     rc = 0
     if rank == 0:
@@ -454,9 +489,12 @@ def main():
                        "causal": causal, "global_batch": B if strong else B * world,
                        "parallelism": (f"(batch,head) units split over {world} GPU(s) (strong), no collective"
                                        if strong else f"(batch,head) shards x{world} (weak), no collective"),
-                       "l2": "inputs (4 x %d MiB per GPU) exceed the 126 MB L2; no flush" % (q.numel() * 2 >> 20)
-                       if q.numel() * 8 > (126 << 20) else "inputs smaller than L2: L2-resident between steps",
-                       "flop_model": "fwd 4BHN^2d*c + bwd 10BHN^2d*c, c=1/2 causal",
+                       "l2": "inputs (4 x %d MiB per GPU per layer) exceed the 126 MB L2; no flush"
+                             % (q.numel() * 2 >> 20) if layers * q.numel() * 8 > (126 << 20)
+                             else "inputs smaller than L2: L2-resident between steps",
+                       "flop_model": "fwd 4BHN^2d*c + bwd 10BHN^2d*c, c=1/2 causal" +
+                                     (f", x {layers} layers per step (one CUDA graph)" if layers > 1 else ""),
+                       "layers": layers,
                        "dropout_p": args.dropout},
             "pct_of_peak": value / world / peak,
             "pct_of_peak_burst": value / world / peak_burst,
@@ -479,7 +517,8 @@ def main():
                          "unit": "TFLOP/s", "frac": achieved / peak, "frac_of_burst": achieved / peak_burst,
                          "frac_of_sustained": achieved / peak_sust, "traffic": traffic,
                          "algorithmic": "8 B H N^2 d c flops per launch (S^T, dP^T, dV, dK GEMMs)"},
-            "e2e": {"value": e2e_val, "unit": "TFLOPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "e2e": {"value": e2e_val, "unit": "TFLOPS", "h2d_bytes_per_step": layers * h2d,
+                    "d2h_bytes_per_step": layers * d2h,
                     "ms_per_step": e2e_ms},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,

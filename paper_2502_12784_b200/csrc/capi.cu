@@ -105,11 +105,17 @@ struct MapCache {
     CUtensorMap map[kSlots];
     bool used[kSlots] = {};
     static size_t slot(const MapKey& k) {
-        size_t h = reinterpret_cast<uintptr_t>(k.ptr) >> 8;
-        h ^= static_cast<size_t>(k.a) * 0x9E3779B97F4A7C15ull ^ static_cast<size_t>(k.b) * 0xC2B2AE3D27D4EB4Full ^
-             static_cast<size_t>(k.c) * 0x165667B19E3779F9ull ^ static_cast<size_t>(k.kind * 2 + k.bf16);
-        h ^= h >> 29;
-        return h % kSlots;
+        // tensors of one call sit at multiples of their (large, power-of-two-ish) size:
+        // mix every address bit into the slot (murmur3 finaliser)
+        uint64_t h = reinterpret_cast<uintptr_t>(k.ptr);
+        h ^= static_cast<uint64_t>(k.a) * 0x9E3779B97F4A7C15ull + static_cast<uint64_t>(k.b) * 0xC2B2AE3D27D4EB4Full +
+             static_cast<uint64_t>(k.c) * 0x165667B19E3779F9ull + static_cast<uint64_t>(k.kind * 2 + k.bf16);
+        h ^= h >> 33;
+        h *= 0xff51afd7ed558ccdull;
+        h ^= h >> 33;
+        h *= 0xc4ceb9fe1a85ec53ull;
+        h ^= h >> 33;
+        return static_cast<size_t>(h % kSlots);
     }
     bool get(const MapKey& k, CUtensorMap* out) {
         std::lock_guard<std::mutex> l(mu);

@@ -246,6 +246,10 @@ __global__ void __launch_bounds__(384, 1)
         const int ntile = t ? nk[1] : nk[0];
         for (int j = 0; j < ntile; ++j) {
             mbar_wait<VATTN_SLEEP_MATH>(s_full + t, j & 1);
+            // O += P V of the previous tile has landed (issued before S(j), so this wait
+            // returns at once): observing every o_done phase in order keeps the parity
+            // waits unambiguous by construction (compute-sanitizer synccheck clean)
+            if (j > 0) mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (j - 1) & 1);
             tc_fence_after();
             stress_delay(1, j);
             if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 0);
@@ -283,8 +287,6 @@ __global__ void __launch_bounds__(384, 1)
                     m_run = m_tile;
                 }
                 l_run *= f;
-                mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (j - 1) & 1);
-                tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < kD / 32; ++c) {
                     uint32_t u[32];

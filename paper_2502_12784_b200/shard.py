@@ -37,13 +37,19 @@ def gather_to_rank0(local: torch.Tensor, bh_total: int, group=None) -> torch.Ten
     rank = dist.get_rank(group)
     sizes = [shard_range(bh_total, world, r) for r in range(world)]
     max_n = max(hi - lo for lo, hi in sizes)
-    pad = torch.zeros((max_n,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    pad[: local.shape[0]] = local
+    # NCCL gathers device tensors in place; gloo (the CPU test path, and the shared-GPU
+    # bench hook) gathers host copies
+    dev = local.device
+    via_host = dist.get_backend(group) == "gloo" and local.is_cuda
+    src = local.cpu() if via_host else local
+    pad = torch.zeros((max_n,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    pad[: src.shape[0]] = src
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
     if rank != 0:
         return None
-    return torch.cat([b[: hi - lo] for b, (lo, hi) in zip(bufs, sizes)], dim=0)
+    out = torch.cat([b[: hi - lo] for b, (lo, hi) in zip(bufs, sizes)], dim=0)
+    return out.to(dev) if via_host else out
 
 
 def run_sharded(fn: Callable[..., Sequence[torch.Tensor]], inputs: Sequence[torch.Tensor], group=None):

@@ -120,3 +120,37 @@ def backward_fused_traffic(cfg) -> TrafficCounter:
     mma = pre_mma + T * (2 * mma_count(br, bc, d) + 2 * mma_count(bc, dp, br) + mma_count(br, dp, bc))
     cvt = pre_cvt + T * 4 * br * bc
     return TrafficCounter(10, 5, BH * reads, BH * writes, BH * mma, 0, BH * cvt)
+
+
+# ------------------------------------------- closed forms vs measured DRAM bytes --
+# the reference's element-traffic closed forms (attention.hpp:40-58,
+# attention_backward.cpp:59-219) turned into BYTES (16-bit tensors 2 B, lse / D and the
+# fp32 dQ partials 4 B) so they can be set beside the DRAM bytes ncu measures for the
+# B200 kernels (profiles/ncu_traffic.json).  The closed forms model a cache-less HBM:
+# every K / V (or Q / dO) tile is re-read for every visited tile pair, so they are the
+# upper bound a kernel reaches only when no tile survives in L2; the algorithmic minimum
+# reads and writes every tensor exactly once.
+
+def fused_forward_hbm_bytes(cfg) -> dict:
+    """Closed-form (cache-less) and minimum HBM bytes of the fused forward."""
+    BH, N, d, br, bc, causal = _dims(cfg)
+    T = visited_pairs(N, br, bc, causal)
+    closed = BH * (2 * (N * d + 2 * bc * d * T) + 2 * N * d + 4 * N)
+    minimum = BH * (2 * 4 * N * d + 4 * N)  # Q, K, V read, O written (16-bit) + lse (f32)
+    return {"closed_form": closed, "minimum": minimum, "visited_pairs_per_bh": T}
+
+
+def fused_backward_hbm_bytes(cfg) -> dict:
+    """Closed-form bytes of the reference's backward without its forward pre-pass (the
+    B200 backward takes O; its D kernel reads O and dO instead): D (N f32) written; per
+    key tile K, V read and dK, dV written; per visited pair Q, dO (16-bit) and lse, D (f32)
+    read and a Br x d fp32 dQ partial reduce-added; dQ finalised (read f32, write 16-bit).
+    Minimum: Q, K, V, O, dO read, dQ, dK, dV written once, lse read, D round trip."""
+    BH, N, d, br, bc, causal = _dims(cfg)
+    T = visited_pairs(N, br, bc, causal)
+    nk = N // bc
+    reads = 2 * (2 * N * d) + 2 * (2 * bc * d * nk) + T * (2 * 2 * br * d + 4 * 2 * br) + 4 * N * d
+    writes = 4 * N + 2 * (2 * bc * d * nk) + T * 4 * br * d + 2 * N * d
+    closed = BH * (reads + writes)
+    minimum = BH * (2 * 5 * N * d + 2 * 3 * N * d + 4 * N + 4 * N * 2)
+    return {"closed_form": closed, "minimum": minimum, "visited_pairs_per_bh": T}

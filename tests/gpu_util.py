@@ -72,3 +72,53 @@ def torch_ref_grads(q, k, v, do, causal, scale=None):
     o = torch.matmul(p, vf)
     o.backward(dof.detach())
     return o.detach(), lse.detach(), qf.grad, kf.grad, vf.grad
+
+
+def softmax_scale32(d: int) -> float:
+    """AttnConfig::scale() in binary32 (attention_forward.cpp:42-45), as the kernels use it."""
+    return float(torch.tensor(1.0, dtype=torch.float32) / torch.sqrt(torch.tensor(float(d), dtype=torch.float32)))
+
+
+def f64_ref(q, k, v, do, causal, scale=None, block=4096):
+    """binary64 restatement of the oracle's attention_ref / attention_grad_ref
+    (reference.cpp:26-167) for ONE (b, h) slice [N, d], run on the GPU in float64 and
+    chunked over query blocks so that N = 32k fits (one 4096 x N block of S at a time).
+    Inputs are the kernels' 16-bit tensors widened exactly.  Returns float64
+    (O, lse, dQ, dK, dV); D = rowsum(dO o O) uses the binary64 O, as the oracle does."""
+    q, k, v, do = (x.double() for x in (q, k, v, do))
+    N, d = q.shape
+    scale = softmax_scale32(d) if scale is None else scale
+    o = torch.empty_like(q)
+    lse = torch.empty(N, dtype=torch.float64, device=q.device)
+    cols = torch.arange(N, device=q.device)
+
+    def scores(r0, r1):
+        s = (q[r0:r1] @ k.T) * scale
+        if causal:
+            rows = torch.arange(r0, r1, device=q.device)[:, None]
+            s = s.masked_fill(cols[None, :] > rows, float("-inf"))
+        return s
+
+    for r0 in range(0, N, block):
+        r1 = min(N, r0 + block)
+        s = scores(r0, r1)
+        m = s.max(dim=1, keepdim=True).values
+        p = torch.exp(s - m)
+        l_ = p.sum(dim=1, keepdim=True)
+        o[r0:r1] = (p @ v) / l_
+        lse[r0:r1] = (m + torch.log(l_)).squeeze(1)
+        del s, p
+    D = (do * o).sum(dim=1)
+    dq = torch.empty_like(q)
+    dk = torch.zeros_like(k)
+    dv = torch.zeros_like(v)
+    for r0 in range(0, N, block):
+        r1 = min(N, r0 + block)
+        p = torch.exp(scores(r0, r1) - lse[r0:r1, None])
+        dv += p.T @ do[r0:r1]
+        ds = p * (do[r0:r1] @ v.T - D[r0:r1, None])
+        del p
+        dq[r0:r1] = (ds @ k) * scale
+        dk += (ds.T @ q[r0:r1]) * scale
+        del ds
+    return o, lse, dq, dk, dv
