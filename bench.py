@@ -397,18 +397,20 @@ def main():
     import ctypes as C
     vb.lib.vattn_profile_enable(1)
     for _ in range(max(3, min(args.steps, 10))):
-        step_eager()
+        step_eager()  # (n_prof steps)
     torch.cuda.synchronize()
     kern_ms = []
-    for kind in (0, 1, 2, 3):  # VATTN_KERNEL_FWD, _BWD_DKDV, _BWD_DQ, _BWD_PRE
+    n_prof = max(3, min(args.steps, 10))
+    for kind in (0, 1, 2, 3, 4):  # VATTN_KERNEL_FWD, _BWD_DKDV, _BWD_DQ, _BWD_PRE, _DROPMASK
         t_ms, n_l = C.c_double(), C.c_int()
         vb.lib.vattn_profile_read(kind, C.byref(t_ms), C.byref(n_l))
-        kern_ms.append(t_ms.value / max(n_l.value, 1))
+        # per launch, except the keep-bit mask: per step (0 without dropout)
+        kern_ms.append(t_ms.value / (n_prof * layers if kind == 4 else max(n_l.value, 1)))
     vb.lib.vattn_profile_enable(0)
     t = torch.tensor([ms] + kern_ms, device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, fwd_ms, dkdv_ms, dq_ms, pre_ms = t.tolist()
+    ms_max, fwd_ms, dkdv_ms, dq_ms, pre_ms, mask_ms = t.tolist()
     ms_step = ms_max / args.steps
     f_unit_fwd, f_unit_bwd = flops(1, 1, N, d, causal)
     f_fwd, f_bwd = n_units_rank * f_unit_fwd, n_units_rank * f_unit_bwd  # one layer of this rank's work
@@ -501,6 +503,7 @@ def main():
             "pct_of_peak_sustained": value / world / peak_sust,
             "peak_used": peak_why,
             "kernels_ms": {"fwd": fwd_ms, "bwd_preprocess": pre_ms, "bwd_dkdv": dkdv_ms, "bwd_dq": dq_ms,
+                           "dropmask": mask_ms,
                            "note": "separate profiled pass after the timed region (CUDA events around each "
                                    "launch, which also break the PDL overlap); the sum can exceed ms_per_step"},
             "fwd_tflops": f_fwd / (fwd_ms * 1e-3) / 1e12,

@@ -119,11 +119,14 @@ int mha_backward(const vattn_config* cfg, const void* q, const void* k, const vo
                  void* workspace, size_t workspace_bytes, void* stream);
 
 /* Dropout keep bits kept from the forward for the backward (optional fast path).
- * mha_dropout_mask_bytes(cfg): size of the mask, B*H*Npad*Npad/8 bytes with Npad = N
- * rounded up to 128 (0 when dropout_p == 0, cfg is invalid, or masks are disabled
- * with VATTN_DROP_MASK=0 -- then both backward kernels hash the bits in place).
- * mha_forward_dropout_mask: mha_forward that also stores the keep bits it computes
- * (query-major, one bit per (query, key) position it visits) into `drop_mask`.
+ * mha_dropout_mask_bytes(cfg): size of the keep-bit mask, 2*B*H*Npad*Npad/8 bytes with
+ * Npad = N rounded up to 128: a query-major copy [unit][query][Npad/32] (bit = key)
+ * followed by a key-major copy [unit][key][Npad/32] (bit = query).  0 when
+ * dropout_p == 0, cfg is invalid, or masks are disabled with VATTN_DROP_MASK=0 (then
+ * every kernel hashes the bits in place).
+ * mha_forward_dropout_mask: mha_forward that first hashes the keep bits of every
+ * visited position into `drop_mask` (one integer-bound kernel, off the softmax's
+ * critical path) and then reads them.
  * mha_backward_dropout_mask: mha_backward that reads those bits instead of hashing
  * the positions again (same results, bit for bit; `drop_mask` must come from
  * mha_forward_dropout_mask with the same cfg).  Both require dropout_p > 0 and a
@@ -200,6 +203,7 @@ void vattn_map_cache_stats(long long* hits, long long* misses);
 #define VATTN_KERNEL_BWD_DKDV 1 /* backward, key-major dK / dV kernel */
 #define VATTN_KERNEL_BWD_DQ 2   /* backward, query-major dQ kernel    */
 #define VATTN_KERNEL_BWD_PRE 3  /* backward preprocess (D, lse2)      */
+#define VATTN_KERNEL_DROPMASK 4 /* dropout keep-bit mask (both copies) */
 void vattn_profile_enable(int on);
 int vattn_profile_read(int kind, double* ms_total, int* launches);
 

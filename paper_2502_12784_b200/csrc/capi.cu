@@ -138,18 +138,36 @@ std::atomic<long long> g_map_hits{0}, g_map_misses{0};
 // [B*H, N, d] 16-bit tensor, 128 rows x 64 columns per box, 128-byte swizzle.
 bool encode_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16) {
     EncodeFn enc = encode_fn();
-    if (!enc) return false;
+    if (!enc) {
+        g_err = "cuTensorMapEncodeTiled: driver entry point unavailable";
+        return false;
+    }
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(N),
                                 static_cast<cuuint64_t>(BH)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2,
                                    static_cast<cuuint64_t>(D) * 2 * static_cast<cuuint64_t>(N)};
     const cuuint32_t box[3] = {64, 128, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r =
-        enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
-            const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    auto encode = [&] {
+        return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    CUresult r = encode();
+    if (r == CUDA_ERROR_INVALID_CONTEXT) {
+        // a host thread that never made the device's primary context current (e.g. the
+        // torch autograd engine's worker thread): the driver call needs one.  Any runtime
+        // call binds it; retry once.
+        cudaFree(nullptr);
+        r = encode();
+    }
+    if (r != CUDA_SUCCESS) {
+        char buf[160];
+        snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (CUresult %d, ptr %p, [%d, %d, %d])", static_cast<int>(r),
+                 ptr, BH, N, D);
+        g_err = buf;
+    }
     return r == CUDA_SUCCESS;
 }
 
@@ -173,9 +191,17 @@ bool encode_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16) 
     const cuuint64_t strides[2] = {256, 32768};
     const cuuint32_t box[3] = {64, 128, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(ptr),
-               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    auto encode = [&] {
+        return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    CUresult r = encode();
+    if (r == CUDA_ERROR_INVALID_CONTEXT) {  // see encode_map
+        cudaFree(nullptr);
+        r = encode();
+    }
+    return r == CUDA_SUCCESS;
 }
 
 bool make_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16) {
@@ -345,6 +371,20 @@ cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, int sme
 }
 
 
+// Both keep-bit copies of `c` (query-major, then key-major; mha_dropmask_kernel).
+void launch_dropmask(const vattn_config* c, uint32_t* mask, cudaStream_t stream) {
+    int H, bh_off;
+    float inv_keep;
+    uint64_t seed, thresh;
+    set_dropout(c, &H, &bh_off, &inv_keep, &seed, &thresh);
+    const int nt = (c->seq_len + 127) / 128;
+    const unsigned pairs = c->causal ? static_cast<unsigned>(nt) * (nt + 1) / 2 : static_cast<unsigned>(nt) * nt;
+    ProfScope prof(stream, 4);
+    const HashMul hm{4u, 32u};  // run-time multipliers (sm100_ptx.cuh, drop_keep_mul)
+    launch_pdl(mha_dropmask_kernel, dim3(pairs, static_cast<unsigned>(units(c))), dim3(256), 0, stream, mask, nt * 128,
+               H, bh_off, seed, thresh, c->causal, hm);
+}
+
 template <int kD, bool kBF16, bool kDrop>
 int launch_forward(const vattn_config* c, const void* q, const void* k, const void* v, void* o,
                    float* lse, uint32_t* drop_mask, unsigned int* status, cudaStream_t stream) {
@@ -352,7 +392,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     CUtensorMap mq, mk, mv, mo;
     if (!make_map(&mq, q, BH, N, kD, kBF16) || !make_map(&mk, k, BH, N, kD, kBF16) ||
         !make_map(&mv, v, BH, N, kD, kBF16) || !make_map(&mo, o, BH, N, kD, kBF16))
-        return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled failed");
+        return fail(VATTN_ECUDA, g_err.empty() ? "cuTensorMapEncodeTiled failed" : g_err);
     auto kern = mha_fwd_sm100_kernel<kD, kBF16, kDrop>;
     constexpr int smem = FwdCfg<kD>::kSmemBytes;
     const cudaError_t attr_err = set_smem_once<mha_fwd_sm100_kernel<kD, kBF16, kDrop>>(smem);
@@ -367,6 +407,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     p.drop_mask = drop_mask;
     p.mask_words = (N + 127) / 128 * 4;
     p.status = status;
+    if (kDrop && drop_mask) launch_dropmask(c, drop_mask, stream);
     const dim3 grid = tile_grid((N + 255) / 256, BH, c->causal ? bh_group(BH, 2ll * N * kD * 2, true) : 1);  // K, V
     {
         ProfScope prof(stream, 0);
@@ -376,7 +417,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     if (e == cudaSuccess) e = g_launch_err;
     g_launch_err = cudaSuccess;
     if (e != cudaSuccess) return fail(VATTN_ECUDA, std::string("mha_fwd launch: ") + cudaGetErrorString(e));
-    g_launches = 1;
+    g_launches = (kDrop && drop_mask) ? 2 : 1;
     return VATTN_OK;
 }
 
@@ -445,7 +486,7 @@ BwdLayout bwd_layout(const vattn_config* c) {
     // dK/dV kernel's row-hash buffer for the dS^T staging box, so dropout takes the dQ
     // GEMM path.  VATTN_DROP_MASK=0: hash in place (and recompute dQ).
     const bool mask_env = drop_mask_enabled();
-    const size_t mask_bytes = BH * static_cast<size_t>(L.Npad) * (L.Npad / 8);
+    const size_t mask_bytes = 2 * BH * static_cast<size_t>(L.Npad) * (L.Npad / 8);  // query- + key-major
     L.drop_mask = c->dropout_p > 0.0f && mask_env;
     L.materialize_ds = c->dropout_p > 0.0f && !L.drop_mask
                            ? false
@@ -469,7 +510,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     if (!make_map(&mq, q, BH, N, kD, kBF16) || !make_map(&mk, k, BH, N, kD, kBF16) ||
         !make_map(&mv, v, BH, N, kD, kBF16) || !make_map(&mdo, dout, BH, N, kD, kBF16) ||
         !make_map(&mdq, dq, BH, N, kD, kBF16))
-        return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled failed");
+        return fail(VATTN_ECUDA, g_err.empty() ? "cuTensorMapEncodeTiled failed" : g_err);
 
     // 1) D = rowsum(dO o O), lse2 = lse * log2(e)
     {
@@ -494,17 +535,18 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     p.ds_tiles_per_bh = L.ds_tiles_per_bh;
     p.tail_units = c->causal ? dkdv_tail_units(BH, L.n_q) : 0;
     p.drop_mask = nullptr;
+    p.drop_mask_k = nullptr;
     bool mask_kernel = false;
     if (L.drop_mask) {
-        if (ext_mask) {  // the forward's own keep bits (mha_forward_dropout_mask)
+        if (ext_mask) {  // the forward's keep bits (mha_forward_dropout_mask)
             p.drop_mask = ext_mask;
         } else {
             uint32_t* m = reinterpret_cast<uint32_t*>(w + L.mask);
             p.drop_mask = m;
             mask_kernel = true;
-            launch_pdl(mha_bwd_dropmask_kernel, dim3(148 * 8), dim3(256), 0, stream, m, L.Npad, BH, p.H, p.bh_off,
-                       p.drop_seed, p.drop_thresh, c->causal);
+            launch_dropmask(c, m, stream);
         }
+        p.drop_mask_k = p.drop_mask + static_cast<size_t>(BH) * L.Npad * (L.Npad / 32);
     }
     CUtensorMap mds;
     if (L.materialize_ds && !make_ds_map(&mds, p.ds_out, static_cast<long long>(BH) * L.ds_tiles_per_bh, kBF16))
@@ -668,7 +710,7 @@ int mha_forward_ex(const vattn_config* cfg, const void* q, const void* k, const 
 size_t mha_dropout_mask_bytes(const vattn_config* cfg) {
     if (validate(cfg) || cfg->dropout_p <= 0.0f || !drop_mask_enabled()) return 0;
     const size_t Npad = static_cast<size_t>((cfg->seq_len + 127) / 128) * 128;
-    return static_cast<size_t>(units(cfg)) * Npad * (Npad / 8);
+    return 2 * static_cast<size_t>(units(cfg)) * Npad * (Npad / 8);  // query-major + key-major copies
 }
 
 int mha_forward_dropout_mask(const vattn_config* cfg, const void* q, const void* k, const void* v, void* o, float* lse,

@@ -89,35 +89,82 @@ struct BwdParams {
     uint16_t* ds_out;
     long long ds_tiles_per_bh;  // n_q^2, or n_q (n_q + 1) / 2 causal (lower triangle)
     int tail_units;             // dK/dV grid: last units dispatched longest-first (grid_item_tail)
-    // Dropout keep bits [unit][query][Npad/32 words] (bit = key), written by the forward
-    // (mha_forward_dropout_mask) or by mha_bwd_dropmask_kernel; nullptr = hash in place.
+    // Dropout keep bits written by mha_dropmask_kernel (nullptr = hash in place):
+    // query-major [unit][query][Npad/32 words] (bit = key) and the key-major copy
+    // [unit][key][Npad/32 words] (bit = query).
     const uint32_t* drop_mask;
+    const uint32_t* drop_mask_k;
 };
 
-// Dropout keep bits of the backward when the forward did not keep them: the
-// reference's position hash (rng.cpp:35-54) evaluated once per position into the
-// query-major mask, instead of inside both backward kernels.  One warp per 32 x 32
-// (query, key) block, lane l = query r0 + l.  Causal: blocks wholly above the diagonal
-// are skipped (those positions are masked; the kernels never use their bits).
-__global__ void __launch_bounds__(256) mha_bwd_dropmask_kernel(uint32_t* __restrict__ mask, int Npad, int BH, int H,
-                                                               int bh_off, uint64_t seed, uint64_t thresh,
-                                                               int causal) {
-    const int W = Npad / 32;
-    const int lane = threadIdx.x & 31;
-    const long long nblk = static_cast<long long>(BH) * W * W;
-    const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+// Dropout keep bits, hashed once per step ahead of the forward: the reference's
+// position hash (rng.cpp:35-54) is data-independent, so it runs in its own
+// integer-bound kernel at full occupancy instead of on the forward's softmax critical
+// path (where it cost ~5 ms at C3).  Two copies, each B*H*Npad^2/8 bytes:
+//   query-major  mask[unit][query][Npad/32]  bit = key    (forward, dQ recompute)
+//   key-major    mask[unit][key][Npad/32]    bit = query  (dK/dV: thread = key row)
+// CTA = one 128 x 128 (query tile, key tile) pair of one (b, h) unit; warp w hashes
+// queries 32 (w & 3) + lane against keys 64 (w >> 2) + [0, 64); 32 ballots per 32 x 32
+// block transpose the bits, staged in shared memory so both copies leave as 16-byte
+// stores.  Causal: tile pairs above the diagonal are skipped (masked positions; no
+// kernel reads their bits).
+__global__ void __launch_bounds__(256) mha_dropmask_kernel(uint32_t* __restrict__ mask, int Npad, int H, int bh_off,
+                                                           uint64_t seed, uint64_t thresh, int causal, HashMul hm) {
+    __shared__ uint32_t qm[128][5];  // [query][key word] (+1 pad)
+    __shared__ uint32_t km[128][5];  // [key][query word]
+    const int nt = Npad / 128, W = Npad / 32;
+    int i, j;  // query tile, key tile
+    const int t = blockIdx.x;
+    if (causal) {  // t -> (i, j <= i), row-major over the lower triangle
+        i = static_cast<int>((sqrtf(8.0f * static_cast<float>(t) + 1.0f) - 1.0f) * 0.5f);
+        while (i * (i + 1) / 2 > t) --i;
+        while ((i + 1) * (i + 2) / 2 <= t) ++i;
+        j = t - i * (i + 1) / 2;
+    } else {
+        i = t / nt;
+        j = t - i * nt;
+    }
+    const int bh = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qs = warp & 3, kh = warp >> 2;
     griddep_wait();
-    for (long long blk = gw; blk < nblk; blk += nw) {
-        const int bh = static_cast<int>(blk / (static_cast<long long>(W) * W));
-        const int rem = static_cast<int>(blk - static_cast<long long>(bh) * W * W);
-        const int rw = rem / W, cw = rem % W;  // query word (row block), key word (column block)
-        if (causal && cw > rw) continue;       // warp-uniform
-        const DropRow dr = drop_row(drop_bh_base(seed, (bh + bh_off) / H, (bh + bh_off) % H), rw * 32 + lane);
+    const DropRow dr = drop_row(drop_bh_base(seed, (bh + bh_off) / H, (bh + bh_off) % H), i * 128 + qs * 32 + lane);
+    const DropThresh th = drop_thresh_split(thresh);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int kw = kh * 2 + c;  // key word within the tile
         uint32_t w = 0;
+        bool any_tie = false;
+        const uint32_t col0 = static_cast<uint32_t>(j * 128 + kw * 32);
 #pragma unroll 8
-        for (int b = 0; b < 32; ++b) w |= static_cast<uint32_t>(drop_keep(dr, cw * 32 + b, thresh)) << b;
-        mask[(static_cast<size_t>(bh) * Npad + rw * 32 + lane) * W + cw] = w;
+        for (int b = 0; b < 32; ++b) {
+            bool tie;
+            w |= static_cast<uint32_t>(drop_keep_mul(dr, col0 + b, th.hi, hm, tie)) << b;
+            any_tie |= tie;
+        }
+        if (any_tie) {  // a high word tied (p ~ 2^-32 per position): redo the word exactly
+            w = 0;
+#pragma unroll 1
+            for (int b = 0; b < 32; ++b) w |= static_cast<uint32_t>(drop_keep(dr, static_cast<int>(col0) + b, thresh)) << b;
+        }
+        qm[qs * 32 + lane][kw] = w;
+        uint32_t tw = 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t col = __ballot_sync(0xffffffffu, (w >> b) & 1u);  // key kw*32+b, bit = query
+            if (lane == b) tw = col;
+        }
+        km[kw * 32 + lane][qs] = tw;
+    }
+    __syncthreads();
+    const size_t base = static_cast<size_t>(bh) * Npad;
+    const size_t half = static_cast<size_t>(gridDim.y) * Npad * W;  // words per copy
+    if (threadIdx.x < 128) {
+        const int r = threadIdx.x;
+        *reinterpret_cast<uint4*>(mask + (base + i * 128 + r) * W + j * 4) = make_uint4(qm[r][0], qm[r][1], qm[r][2], qm[r][3]);
+    } else {
+        const int r = threadIdx.x - 128;
+        *reinterpret_cast<uint4*>(mask + half + (base + j * 128 + r) * W + i * 4) =
+            make_uint4(km[r][0], km[r][1], km[r][2], km[r][3]);
     }
     griddep_launch_dependents();
 }
@@ -370,6 +417,10 @@ __global__ void __launch_bounds__(384, 1)
             const float* lse2 = sLD + st * 256 + 64 * h;
             const float* dsum = sLD + st * 256 + 128 + 64 * h;
             const uint32_t sR = Cfg::kTmemS + (kDB ? (s & 1) * 128u : 0u);  // S / P^T region of this tile
+            uint2 kmw = make_uint2(~0u, ~0u);
+            if (kDrop && p.drop_mask_k)  // this key row's 64 query bits, key-major copy (mha_dropmask_kernel)
+                kmw = __ldg(reinterpret_cast<const uint2*>(
+                    p.drop_mask_k + (static_cast<size_t>(bh) * p.Npad + key) * (p.Npad / 32) + i * 4 + 2 * h));
             mbar_wait(q_full + st, (s / kSt) & 1);  // lse2 / D of this tile landed
             mbar_wait(s_full + (kDB ? (s & 1) : 0), kDB ? ((s >> 1) & 1) : (s & 1));
             tc_fence_after();
@@ -381,24 +432,8 @@ __global__ void __launch_bounds__(384, 1)
             tmem_wait_ld();
             const int qbase = i * 128 + 64 * h;
             uint64_t keepm = ~0ull;  // dropout keep bits of this thread's 64 (query, key) positions
-            if (kDrop && p.drop_mask) {
-                // 64 query bits of this key row out of the query-major mask: lane l reads
-                // the words of queries qbase + l and qbase + 32 + l for this warp's 32 keys,
-                // 32 ballot pairs transpose them (lane b keeps key b's query bits)
-                const int W = p.Npad / 32;
-                const uint32_t* mw = p.drop_mask + (static_cast<size_t>(bh) * p.Npad + qbase) * W + kb * 4 + (warp & 3);
-                const uint32_t w0 = mw[static_cast<size_t>(lane) * W], w1 = mw[static_cast<size_t>(lane + 32) * W];
-                uint32_t t0 = 0, t1 = 0;
-#pragma unroll
-                for (int b = 0; b < 32; ++b) {
-                    const uint32_t b0 = __ballot_sync(0xffffffffu, (w0 >> b) & 1u);
-                    const uint32_t b1 = __ballot_sync(0xffffffffu, (w1 >> b) & 1u);
-                    if (lane == b) {
-                        t0 = b0;
-                        t1 = b1;
-                    }
-                }
-                keepm = static_cast<uint64_t>(t0) | (static_cast<uint64_t>(t1) << 32);
+            if (kDrop && p.drop_mask_k) {
+                keepm = static_cast<uint64_t>(kmw.x) | (static_cast<uint64_t>(kmw.y) << 32);
             } else if constexpr (kDrop) {
                 // row prefixes of the reference hash for this warpgroup's 64 queries
                 named_bar_sync(1 + h, 128);  // previous step's readers are done
@@ -406,8 +441,8 @@ __global__ void __launch_bounds__(384, 1)
                     sDrop[64 * h + (warp & 3) * 32 + lane] = drop_row(dbase, qbase + (warp & 3) * 32 + lane);
                 named_bar_sync(1 + h, 128);
                 keepm = 0;
-#pragma unroll
-                for (int x = 0; x < 64; ++x)
+#pragma unroll 1
+                for (int x = 0; x < 64; ++x)  // (fallback without a mask: kept out of the i-cache)
                     keepm |= static_cast<uint64_t>(drop_keep(sDrop[64 * h + x], key, p.drop_thresh)) << x;
             }
             // P = exp2(S c - lse2).  The two warpgroups exponentiate at the same time on
@@ -445,10 +480,12 @@ __global__ void __launch_bounds__(384, 1)
             {
                 uint32_t pk[32];
                 if constexpr (kDrop) {  // dV operand f16(P * drop) (attention_backward.cpp:163-167)
+                    const float2 ik2 = make_float2(p.inv_keep, p.inv_keep);
 #pragma unroll
-                    for (int x = 0; x < 32; ++x)
-                        pk[x] = pack2<kBF16>((keepm >> (2 * x)) & 1 ? pr[2 * x] * p.inv_keep : 0.0f,
-                                             (keepm >> (2 * x + 1)) & 1 ? pr[2 * x + 1] * p.inv_keep : 0.0f);
+                    for (int x = 0; x < 32; ++x) {
+                        const float2 pd = fmul2(make_float2(pr[2 * x], pr[2 * x + 1]), ik2);  // packed FMUL2
+                        pk[x] = pack2<kBF16>((keepm >> (2 * x)) & 1 ? pd.x : 0.0f, (keepm >> (2 * x + 1)) & 1 ? pd.y : 0.0f);
+                    }
                 } else {
 #pragma unroll
                     for (int x = 0; x < 32; ++x) pk[x] = pack2<kBF16>(pr[2 * x], pr[2 * x + 1]);
@@ -474,17 +511,25 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int x = 0; x < 32; x += 4) {
                     const float4 d4 = *reinterpret_cast<const float4*>(dsum + 32 * c + x);
-                    float dpd[4] = {dpv[x], dpv[x + 1], dpv[x + 2], dpv[x + 3]};
-                    if constexpr (kDrop) {  // dS = P o (drop o dP - D) (attention_backward.cpp:176-182)
-#pragma unroll
-                        for (int y = 0; y < 4; ++y)
-                            dpd[y] = (keepm >> (32 * c + x + y)) & 1 ? dpd[y] * p.inv_keep : 0.0f;
+                    float2 t0, t1;  // dP - D, packed FADD2 / FMUL2: half the issue slots
+                    if constexpr (kDrop) {
+                        // dS = P o (drop o dP - D) (attention_backward.cpp:176-182): one FFMA2
+                        // dP * 1/(1-p) - D per pair, then -D where the position was dropped
+                        const float2 ik2 = make_float2(p.inv_keep, p.inv_keep);
+                        const float2 nd0 = make_float2(-d4.x, -d4.y), nd1 = make_float2(-d4.z, -d4.w);
+                        t0 = ffma2(make_float2(dpv[x], dpv[x + 1]), ik2, nd0);
+                        t1 = ffma2(make_float2(dpv[x + 2], dpv[x + 3]), ik2, nd1);
+                        const int b = 32 * c + x;
+                        t0.x = (keepm >> b) & 1 ? t0.x : nd0.x;
+                        t0.y = (keepm >> (b + 1)) & 1 ? t0.y : nd0.y;
+                        t1.x = (keepm >> (b + 2)) & 1 ? t1.x : nd1.x;
+                        t1.y = (keepm >> (b + 3)) & 1 ? t1.y : nd1.y;
+                    } else {
+                        t0 = fadd2(make_float2(dpv[x], dpv[x + 1]), make_float2(-d4.x, -d4.y));
+                        t1 = fadd2(make_float2(dpv[x + 2], dpv[x + 3]), make_float2(-d4.z, -d4.w));
                     }
-                    // packed FADD2 / FMUL2: half the issue slots
-                    const float2 s0 = fmul2(make_float2(pr[32 * c + x], pr[32 * c + x + 1]),
-                                            fadd2(make_float2(dpd[0], dpd[1]), make_float2(-d4.x, -d4.y)));
-                    const float2 s1 = fmul2(make_float2(pr[32 * c + x + 2], pr[32 * c + x + 3]),
-                                            fadd2(make_float2(dpd[2], dpd[3]), make_float2(-d4.z, -d4.w)));
+                    const float2 s0 = fmul2(make_float2(pr[32 * c + x], pr[32 * c + x + 1]), t0);
+                    const float2 s1 = fmul2(make_float2(pr[32 * c + x + 2], pr[32 * c + x + 3]), t1);
                     dsp[16 * c + x / 2] = pack2<kBF16>(s0.x, s0.y);
                     dsp[16 * c + x / 2 + 1] = pack2<kBF16>(s1.x, s1.y);
                 }
@@ -854,26 +899,35 @@ __global__ void __launch_bounds__(384, 1)
                     tmem_ld32f(tmem + lb + Cfg::kTmemDP + 64 * h + 32 * c, dpb);
                     tmem_wait_ld();
                 }
-                if constexpr (kDrop) {  // dS = P o (drop o dP - D)
-                    if (p.drop_mask) {
-                        const uint32_t kw = p.drop_mask[(static_cast<size_t>(bh) * p.Npad + q) * (p.Npad / 32) +
-                                                        (j * 128 + 64 * h + 32 * c) / 32];
-#pragma unroll
-                        for (int x = 0; x < 32; ++x) dpv[x] = (kw >> x) & 1u ? dpv[x] * p.inv_keep : 0.0f;
-                    } else {
-#pragma unroll
-                        for (int x = 0; x < 32; ++x) {
-                            const int col = j * 128 + 64 * h + 32 * c + x;
-                            dpv[x] = drop_keep(drow, col, p.drop_thresh) ? dpv[x] * p.inv_keep : 0.0f;
-                        }
-                    }
-                }
                 const float2 nd2 = make_float2(-dsum, -dsum);
+                if constexpr (kDrop) {
+                    // dS = P o (drop o dP - D), the dK/dV kernel's arithmetic exactly: one FFMA2
+                    // dP * 1/(1-p) - D per pair, -D where the position was dropped
+                    uint32_t kw;
+                    if (p.drop_mask) {
+                        kw = p.drop_mask[(static_cast<size_t>(bh) * p.Npad + q) * (p.Npad / 32) + (j * 128 + 64 * h + 32 * c) / 32];
+                    } else {
+                        kw = 0;
+#pragma unroll 1
+                        for (int x = 0; x < 32; ++x)
+                            kw |= static_cast<uint32_t>(drop_keep(drow, j * 128 + 64 * h + 32 * c + x, p.drop_thresh)) << x;
+                    }
+                    const float2 ik2 = make_float2(p.inv_keep, p.inv_keep);
 #pragma unroll
-                for (int x = 0; x < 16; ++x) {  // packed FADD2 / FMUL2: half the issue slots
-                    const float2 ds = fmul2(make_float2(pr[32 * c + 2 * x], pr[32 * c + 2 * x + 1]),
-                                            fadd2(make_float2(dpv[2 * x], dpv[2 * x + 1]), nd2));
-                    dsp[16 * c + x] = pack2<kBF16>(ds.x, ds.y);
+                    for (int x = 0; x < 16; ++x) {
+                        float2 t = ffma2(make_float2(dpv[2 * x], dpv[2 * x + 1]), ik2, nd2);
+                        t.x = (kw >> (2 * x)) & 1u ? t.x : nd2.x;
+                        t.y = (kw >> (2 * x + 1)) & 1u ? t.y : nd2.y;
+                        const float2 ds = fmul2(make_float2(pr[32 * c + 2 * x], pr[32 * c + 2 * x + 1]), t);
+                        dsp[16 * c + x] = pack2<kBF16>(ds.x, ds.y);
+                    }
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) {  // packed FADD2 / FMUL2: half the issue slots
+                        const float2 ds = fmul2(make_float2(pr[32 * c + 2 * x], pr[32 * c + 2 * x + 1]),
+                                                fadd2(make_float2(dpv[2 * x], dpv[2 * x + 1]), nd2));
+                        dsp[16 * c + x] = pack2<kBF16>(ds.x, ds.y);
+                    }
                 }
             }
             tmem_st32(tmem + lb + R + 64 * h, dsp);  // dS over our (consumed) S columns

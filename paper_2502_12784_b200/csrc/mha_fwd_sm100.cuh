@@ -37,9 +37,10 @@ struct FwdParams {
     float inv_keep;      // 1 / (1 - dropout_p), binary32 like the reference
     uint64_t drop_seed;
     uint64_t drop_thresh;  // keep iff (hash >> 11) >= drop_thresh
-    // optional: the keep bits as computed, [unit][query][Npad/32] words (bit = key), for
-    // the backward (mha_forward_dropout_mask); nullptr = not kept
-    uint32_t* drop_mask;
+    // optional: the keep bits, query-major [unit][query][Npad/32] words (bit = key), hashed
+    // ahead of the forward by mha_dropmask_kernel (mha_forward_dropout_mask); nullptr =
+    // hash every position here
+    const uint32_t* drop_mask;
     int mask_words;        // Npad / 32
     // optional device word: bit VATTN_DOMAIN_ROW (1) is OR-ed in when a query row had a
     // NaN / +inf score or an empty softmax sum (l == 0), the reference's domain_error
@@ -253,6 +254,10 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_after();
             stress_delay(1, j);
             if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 0);
+            uint4 kw4 = make_uint4(0u, 0u, 0u, 0u);  // this row's keep bits of key tile j
+            if (kDrop && p.drop_mask && row < p.mask_words * 32)
+                kw4 = __ldg(reinterpret_cast<const uint4*>(p.drop_mask + (static_cast<size_t>(bh) * p.mask_words * 32 + row) *
+                                                                             p.mask_words + j * 4));
             float s[128];
             tmem_ld32f(tS + 0, s);
             tmem_ld32f(tS + 32, s + 32);
@@ -307,7 +312,13 @@ __global__ void __launch_bounds__(384, 1)
             // of quarter q completes (wait::st) while quarter q+1 is computed, so
             // the store latency never sits on the softmax's critical path.
             auto quarter = [&](int qq, uint32_t (&pk)[16], auto poly_pair) {
-                uint32_t kbits = 0;  // keep bits of this quarter's 32 keys
+                uint32_t kw = qq == 0 ? kw4.x : qq == 1 ? kw4.y : qq == 2 ? kw4.z : kw4.w;
+                if (kDrop && !p.drop_mask) {  // no pre-hashed bits: hash this quarter's 32 keys here
+                    kw = 0;
+#pragma unroll 1
+                    for (int b = 0; b < 32; ++b)
+                        kw |= static_cast<uint32_t>(drop_keep(drow, j * 128 + 32 * qq + b, p.drop_thresh)) << b;
+                }
 #pragma unroll
                 for (int x = 0; x < 16; ++x) {
                     const int c = 32 * qq + 2 * x;
@@ -324,19 +335,12 @@ __global__ void __launch_bounds__(384, 1)
                     if constexpr (kDrop) {
                         // dropout on the 16-bit P: f16(f16(P) * 1/(1-p)) or 0
                         // (attention_forward.cpp:94-106)
-                        const int col = j * 128 + c;
                         const float2 f = unpack2<kBF16>(pk[x]);
-                        const bool k0 = drop_keep(drow, col, p.drop_thresh), k1 = drop_keep(drow, col + 1, p.drop_thresh);
-                        kbits |= (static_cast<uint32_t>(k0) | (static_cast<uint32_t>(k1) << 1)) << (2 * x);
+                        const bool k0 = (kw >> (2 * x)) & 1u, k1 = (kw >> (2 * x + 1)) & 1u;
                         pk[x] = pack2<kBF16>(k0 ? f.x * p.inv_keep : 0.0f, k1 ? f.y * p.inv_keep : 0.0f);
                     }
                 }
-                (void)kbits;
-                if constexpr (kDrop) {
-                    if (p.drop_mask)
-                        p.drop_mask[(static_cast<size_t>(bh) * p.mask_words * 32 + row) * p.mask_words + j * 4 + qq] =
-                            kbits;
-                }
+                (void)kw;
             };
             auto publish = [&](int qq) {  // quarter qq's tcgen05.st has been waited on
                 tc_fence_before();

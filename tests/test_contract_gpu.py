@@ -142,3 +142,35 @@ def test_two_devices_one_process():
         res.append([t.cpu() for t in (o, lse) + tuple(g)])
     for a, b in zip(*res):
         assert torch.equal(a, b)
+
+
+def test_fresh_host_thread_without_current_context():
+    """A host thread that never made the primary context current (the torch autograd
+    engine's worker thread is one) still encodes its TMA descriptors: the first
+    cuTensorMapEncodeTiled there returns CUDA_ERROR_INVALID_CONTEXT, the C ABI binds
+    the context and retries.  Fresh shapes so the descriptor cache misses."""
+    import threading
+
+    q, k, v, do = _inputs(B=1, H=3, N=333, d=128, dtype=torch.bfloat16, seed=7)
+    o_ref, l_ref = vb.mha_forward(q, k, v, True)
+    g_ref = vb.mha_backward(q, k, v, o_ref, do, l_ref, True)
+    q2, k2, v2, do2 = (t.clone() for t in (q, k, v, do))  # new pointers: cache misses in the thread
+    torch.cuda.synchronize()
+    out = {}
+
+    def run():
+        try:
+            o, l = vb.mha_forward(q2, k2, v2, True)
+            out["g"] = vb.mha_backward(q2, k2, v2, o, do2, l, True)
+            out["o"] = o
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001 -- re-raised on the main thread
+            out["err"] = e
+
+    t = threading.Thread(target=run)
+    t.start()
+    t.join()
+    assert "err" not in out, out.get("err")
+    assert torch.equal(out["o"], o_ref)
+    for a, b in zip(out["g"], g_ref):
+        assert torch.equal(a, b)

@@ -364,15 +364,18 @@ def test_forward_dropout_mask_bits_and_backward_bitwise(B, H, N, d, causal, dtyp
     g0 = vb.mha_backward(q, k, v, o0, do, l0, causal, dropout_p=p, seed=seed)
     for name, a, b in zip(("dq", "dk", "dv"), g1, g0):
         assert torch.equal(a, b), name
-    # the bits themselves, on a sample of rows (bit = key of the query's row words)
+    # the bits themselves, on a sample of rows: the query-major copy (bit = key of the
+    # query's row words) and the key-major copy (bit = query of the key's row words)
     npad = (N + 127) // 128 * 128
-    words = m.view(torch.int32).view(B * H, npad, npad // 32).cpu().numpy().view(np.uint32)
+    words = m.view(torch.int32).view(2, B * H, npad, npad // 32).cpu().numpy().view(np.uint32)
     for u in range(B * H):
         for row in (0, N // 2, N - 1):
             cols = range(row + 1) if causal else range(N)
-            want = [po.dropout_keep(seed, u // H, u % H, row, c, p) for c in cols]
-            got = [(words[u, row, c // 32] >> (c % 32)) & 1 for c in cols]
-            assert got == [int(x) for x in want], (u, row)
+            want = [int(po.dropout_keep(seed, u // H, u % H, row, c, p)) for c in cols]
+            got = [(words[0, u, row, c // 32] >> (c % 32)) & 1 for c in cols]
+            assert got == want, (u, row)
+            got_k = [(words[1, u, c, row // 32] >> (row % 32)) & 1 for c in cols]
+            assert got_k == want, ("key-major", u, row)
 
 
 def test_autograd_dropout_uses_forward_mask():
