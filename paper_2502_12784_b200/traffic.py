@@ -154,3 +154,35 @@ def fused_backward_hbm_bytes(cfg) -> dict:
     closed = BH * (reads + writes)
     minimum = BH * (2 * 5 * N * d + 2 * 3 * N * d + 4 * N + 4 * N * 2)
     return {"closed_form": closed, "minimum": minimum, "visited_pairs_per_bh": T}
+
+
+def b200_hbm_model(cfg) -> dict:
+    """Per-kernel DRAM bytes of the B200 path (d = 128 dS-materialised backward) under two
+    caching extremes, for the cross-check against ncu (tools/traffic_crosscheck.py):
+
+    * ``l2_reuse``: every tensor crosses HBM exactly once per kernel (K / V / Q / dO
+      re-reads across CTAs all hit the 126 MB L2) -- the kernel's algorithmic bytes,
+      plus the dS^T tiles the dK/dV kernel writes and the dQ GEMM reads back (16-bit,
+      128 x 128 per visited (query tile, key tile) pair);
+    * ``cache_less``: the reference's closed-form accounting (attention.hpp:40-58):
+      every visited tile pair re-reads its streamed operand tiles from HBM.
+
+    Tile sizes are the B200 kernels' own: the forward CTA covers 256 query rows against
+    128-key tiles, the backward 128 x 128."""
+    BH, N, d = cfg.batch * cfg.heads, cfg.seq_len, cfg.head_dim
+    causal = bool(cfg.causal)
+    T = visited_pairs(N, 128, 128, causal)           # backward tile pairs per (b, h)
+    Tf = visited_pairs(N, 256, 128, causal)          # forward (256-row CTA) pairs per (b, h)
+    nd2 = 2 * N * d                                  # one 16-bit [N, d] tensor
+    ds = T * 128 * 128 * 2
+    out = {
+        "fwd": {"l2_reuse": BH * (4 * nd2 + 4 * N),                       # Q, K, V in, O out, lse
+                "cache_less": BH * (nd2 + Tf * 2 * 128 * d * 2 + nd2 + 4 * N)},
+        "bwd_preprocess": {"l2_reuse": BH * (2 * nd2 + 4 * N + 8 * N),    # O, dO, lse in; D, lse2 out
+                           "cache_less": BH * (2 * nd2 + 4 * N + 8 * N)},
+        "bwd_dkdv": {"l2_reuse": BH * (4 * nd2 + 8 * N + 2 * nd2 + ds),   # K V Q dO, lse2 D, dK dV, dS^T
+                     "cache_less": BH * (2 * nd2 + T * (2 * 128 * d * 2 + 8 * 128) + 2 * nd2 + ds)},
+        "bwd_dq_gemm": {"l2_reuse": BH * (ds + nd2 + nd2),                # dS^T, K in; dQ out
+                        "cache_less": BH * (ds + T * 128 * d * 2 + nd2)},
+    }
+    return out

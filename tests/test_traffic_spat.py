@@ -96,3 +96,24 @@ def test_spat_errors_match_reference(tmp_path):
             spat.read_spat(p)
     with pytest.raises(ValueError):
         spat.write_spat(str(tmp_path / "bf.spat"), torch.zeros(2, dtype=torch.bfloat16))
+
+
+def test_f4_closed_forms_bracket_ncu_dram_bytes():
+    """the measured DRAM bytes of every B200 kernel (profiles/ncu_traffic.json,
+    one ncu --set full launch each) lie between 'every tensor once' (minus 2 % for ncu's
+    sector granularity) and the reference's cache-less closed form (attention.hpp:40-58)."""
+    import json
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "tools"))
+    import traffic_crosscheck as tc
+    meas = json.load(open(os.path.join(root, "profiles", "ncu_traffic.json")))["c3"]
+    for name, once, cache_less, got in tc.rows(meas):
+        assert got is not None, name
+        assert 0.98 * once <= got <= max(cache_less, once) * 1.02, (name, once, cache_less, got)
+    # the dS^T round trip: the dK/dV kernel and the dQ GEMM move what the model says
+    r = {n: (o, g) for n, o, _, g in tc.rows(meas)}
+    for k in ("bwd_dkdv", "bwd_dq_gemm"):
+        o, g = r[k]
+        assert abs(g / o - 1) < 0.03, (k, g / o)
