@@ -515,8 +515,10 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     // 1) D = rowsum(dO o O), lse2 = lse * log2(e)
     {
         const long long rows = static_cast<long long>(BH) * L.Npad;
-        long long blocks = (rows + 7) / 8;
-        if (blocks > 148 * 16) blocks = 148 * 16;
+        // one wave (8 x 256-thread blocks per SM), each warp 4 x (32 / (d / 8)) rows per pass
+        const long long rows_per_block = 8ll * 4 * (256 / kD);
+        long long blocks = (rows + rows_per_block - 1) / rows_per_block;
+        if (blocks > 148 * 8) blocks = 148 * 8;
         ProfScope prof(stream, 3);
         launch_pdl(mha_bwd_preprocess_kernel<kD, kBF16>, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream,
                    o, dout, lse, lse2, dsum, N, L.Npad, BH);

@@ -36,36 +36,49 @@ __global__ void __launch_bounds__(256) mha_bwd_preprocess_kernel(
     using T16 = typename std::conditional<kBF16, __nv_bfloat16, __half>::type;
     constexpr int kLanesPerRow = kD / 8;
     constexpr int kRowsPerWarp = 32 / kLanesPerRow;
+    constexpr int kU = 4;  // rows per thread per iteration: 2 * kU 16-byte loads in flight
     const int lane = threadIdx.x & 31;
     const int sub = lane % kLanesPerRow;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const long long rows = static_cast<long long>(BH) * Npad;
     griddep_wait();  // O / lse come from the forward kernel
-    for (long long r0 = static_cast<long long>(gw) * kRowsPerWarp; r0 < rows;
-         r0 += static_cast<long long>(nwarps) * kRowsPerWarp) {
-        const long long row = r0 + lane / kLanesPerRow;
-        const int bh = static_cast<int>(row / Npad);
-        const int n = static_cast<int>(row - static_cast<long long>(bh) * Npad);
-        const bool valid = row < rows && n < N;
-        float acc = 0.0f;
-        if (valid) {
-            const size_t base = (static_cast<size_t>(bh) * N + n) * kD + sub * 8;
-            const uint4 a = *reinterpret_cast<const uint4*>(reinterpret_cast<const T16*>(o) + base);
-            const uint4 g = *reinterpret_cast<const uint4*>(reinterpret_cast<const T16*>(dout) + base);
-            const uint32_t av[4] = {a.x, a.y, a.z, a.w}, gv[4] = {g.x, g.y, g.z, g.w};
+    for (long long r0 = static_cast<long long>(gw) * kRowsPerWarp * kU; r0 < rows;
+         r0 += static_cast<long long>(nwarps) * kRowsPerWarp * kU) {
+        long long row[kU];
+        int bh[kU], n[kU];
+        bool valid[kU];
+        uint4 a[kU], g[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            row[u] = r0 + u * kRowsPerWarp + lane / kLanesPerRow;
+            bh[u] = static_cast<int>(row[u] / Npad);
+            n[u] = static_cast<int>(row[u] - static_cast<long long>(bh[u]) * Npad);
+            valid[u] = row[u] < rows && n[u] < N;
+            a[u] = g[u] = make_uint4(0u, 0u, 0u, 0u);
+            if (valid[u]) {
+                const size_t base = (static_cast<size_t>(bh[u]) * N + n[u]) * kD + sub * 8;
+                a[u] = *reinterpret_cast<const uint4*>(reinterpret_cast<const T16*>(o) + base);
+                g[u] = *reinterpret_cast<const uint4*>(reinterpret_cast<const T16*>(dout) + base);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t av[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, gv[4] = {g[u].x, g[u].y, g[u].z, g[u].w};
+            float acc = 0.0f;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const float2 x = unpack2<kBF16>(av[e]), y = unpack2<kBF16>(gv[e]);
                 acc = fmaf(y.x, x.x, acc);
                 acc = fmaf(y.y, x.y, acc);
             }
-        }
 #pragma unroll
-        for (int off = kLanesPerRow / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (sub == 0 && row < rows) {
-            dsum[row] = valid ? acc : 0.0f;
-            if (lse2) lse2[row] = valid ? lse[static_cast<size_t>(bh) * N + n] * 1.4426950408889634f : INFINITY;
+            for (int off = kLanesPerRow / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (sub == 0 && row[u] < rows) {
+                dsum[row[u]] = valid[u] ? acc : 0.0f;
+                if (lse2)
+                    lse2[row[u]] = valid[u] ? lse[static_cast<size_t>(bh[u]) * N + n[u]] * 1.4426950408889634f : INFINITY;
+            }
         }
     }
     griddep_launch_dependents();

@@ -103,7 +103,8 @@ def launches(path: str) -> list:
 
 def main():
     d, tag, cfg = sys.argv[1], sys.argv[2], sys.argv[3]
-    prof = os.path.join(ROOT, "profiles")
+    prof = os.environ.get("VATTN_PROFILES_DIR", os.path.join(ROOT, "profiles"))  # (gpurun: a dir under gpurun_out)
+    os.makedirs(prof, exist_ok=True)
     gpu = open(os.path.join(d, "gpu.txt")).read().strip().splitlines()[-1] if os.path.exists(os.path.join(d, "gpu.txt")) else ""
     # ---- launch list
     lp = os.path.join(d, "launches.csv")
