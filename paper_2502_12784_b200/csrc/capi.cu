@@ -560,7 +560,8 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
-        launch_pdl(kern, dim3(L.n_q * BH), dim3(384), smem, stream, mq, mk, mv, mdo, L.materialize_ds ? mds : mq, dk, dv,
+        launch_pdl(kern, dim3(L.n_q * BH), dim3(DkdvCfg<kD>::kThreads), smem, stream, mq, mk, mv, mdo,
+                   L.materialize_ds ? mds : mq, dk, dv,
                    p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)

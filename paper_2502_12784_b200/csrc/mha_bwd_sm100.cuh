@@ -49,11 +49,19 @@ __global__ void __launch_bounds__(256) mha_bwd_preprocess_kernel(
         int bh[kU], n[kU];
         bool valid[kU];
         uint4 a[kU], g[kU];
+        // one division per pass (the pass's rows are consecutive; a row past the end of a
+        // head moves to the next)
+        const int bh0 = static_cast<int>(r0 / Npad);
+        const int n0 = static_cast<int>(r0 - static_cast<long long>(bh0) * Npad);
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             row[u] = r0 + u * kRowsPerWarp + lane / kLanesPerRow;
-            bh[u] = static_cast<int>(row[u] / Npad);
-            n[u] = static_cast<int>(row[u] - static_cast<long long>(bh[u]) * Npad);
+            bh[u] = bh0;
+            n[u] = n0 + u * kRowsPerWarp + lane / kLanesPerRow;
+            while (n[u] >= Npad) {  // at most once unless Npad < 32 / (d / 8) * 4 (mha_dpsum, tiny N)
+                n[u] -= Npad;
+                ++bh[u];
+            }
             valid[u] = row[u] < rows && n[u] < N;
             a[u] = g[u] = make_uint4(0u, 0u, 0u, 0u);
             if (valid[u]) {
@@ -203,9 +211,29 @@ VATTN_DEV long long ds_tile_index(const BwdParams& p, int i, int kb) {
 // d = 64 frees tensor memory for a second S^T region: S_(i+2) is computed while
 // the P pass of tile i+1 runs, so the P pass never waits for S (with a third Q/dO
 // stage so the load of Q_(i+2) does not wait for dK_i).  d = 128 keeps one region.
+// Math warpgroups of the dK/dV kernel (2: 64 query columns each; 4: 32 each, 640
+// threads).  Measured (profiles/r2_experiments.md): 4 is slower at both head dims --
+// d = 64 +6..14 %, d = 128 (C3) +11 % per dK/dV launch -- the step is not bound by the
+// math warps' latency, so the knobs stay at 2.
+#ifndef VATTN_DKDV64_WG
+#define VATTN_DKDV64_WG 2
+#endif
+#ifndef VATTN_DKDV128_WG
+#define VATTN_DKDV128_WG 2
+#endif
 template <int kD>
 struct DkdvCfg {
     static constexpr bool kDoubleS = kD == 64;
+    static constexpr int kWG = kD == 64 ? VATTN_DKDV64_WG : VATTN_DKDV128_WG;  // math warpgroups
+    static constexpr int kQW = 128 / kWG;                        // query columns per warpgroup
+    static constexpr int kHalves = kQW == 64 ? 2 : 1;            // P^T publication chunks per warpgroup
+    static constexpr int kThreads = 128 + 128 * kWG;
+    // register split (setmaxnreg): producer / MMA / allocator warps vs math warps.  The
+    // split redistributes the CTA's launch allocation (kThreads x the launch-bound
+    // register count: 168 at 384 threads, 96 at 640), so 128 lo + 128 kWG hi must fit it.
+    static constexpr uint32_t kRegsLo = kWG == 2 ? 88 : 56;
+    static constexpr uint32_t kRegsHi = kWG == 2 ? 208 : 104;
+    static_assert(128 * kRegsLo + 128 * kWG * kRegsHi <= kThreads * (kWG == 2 ? 168 : 96), "register split");
     static constexpr int kTileBytes = kD * 128 * 2;
     static constexpr int kBoxes = kD / 64;
     static constexpr int kStages = kDoubleS ? 3 : 2;
@@ -220,7 +248,7 @@ struct DkdvCfg {
     // bits are hashed in place (no keep-bit mask) -- and then materialisation is off.
     static constexpr int kSmemDsStage = kSmemDrop;
     static constexpr int kSmemBar = kSmemDsStage + 32768;
-    static constexpr int kNumBars = 20;
+    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 1 + 2 * kWG * kHalves + kWG + 1;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr uint32_t kTmemS = 0;                       // region r at 128 r
     static constexpr uint32_t kTmemDP = kDoubleS ? 256 : 128;
@@ -228,7 +256,7 @@ struct DkdvCfg {
 };
 
 template <int kD, bool kBF16, bool kDrop>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
     mha_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v,
@@ -262,9 +290,13 @@ __global__ void __launch_bounds__(384, 1)
     // and the early arrival can complete phase s before a slow warp of the same
     // warpgroup wrote its rows (race).  Two barriers keep every phase distinct: a
     // warpgroup can never run two steps ahead (dP_(s+1) needs dK_s, i.e. all of dS_s).
-    uint64_t* p_full = dp_full + 1;   // [2][warpgroup]
-    uint64_t* ds_full = p_full + 4;   // [warpgroup]
-    uint64_t* dkv_full = ds_full + 2;
+    // With 64 query columns a warpgroup publishes its P^T in two 32-query halves
+    // (p_full[s & 1][wg][half]): the dV MMA starts on the first half while the second is
+    // exponentiated.
+    constexpr int kWG = Cfg::kWG, kQW = Cfg::kQW, kHv = Cfg::kHalves;
+    uint64_t* p_full = dp_full + 1;              // [2][warpgroup][half]
+    uint64_t* ds_full = p_full + 2 * kWG * kHv;  // [warpgroup]
+    uint64_t* dkv_full = ds_full + kWG;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
     const int warp = warp_id();
@@ -281,13 +313,13 @@ __global__ void __launch_bounds__(384, 1)
         mbar_init(kv_full, 1);
         for (int s = 0; s < kSt; ++s) {
             mbar_init(q_full + s, 1);
-            mbar_init(q_empty + s, 1 + 8);  // MMA commit + 8 warps done with lse2/D
+            mbar_init(q_empty + s, 1 + 4 * kWG);  // MMA commit + every math warp done with lse2/D
         }
         mbar_init(s_full, 1);
         if (kDB) mbar_init(s_full + 1, 1);
         mbar_init(dp_full, 1);
-        for (int x = 0; x < 4; ++x) mbar_init(p_full + x, 4);  // one arrive per warp of warpgroup x & 1
-        for (int x = 0; x < 2; ++x) mbar_init(ds_full + x, 4);
+        for (int x = 0; x < 2 * kWG * kHv; ++x) mbar_init(p_full + x, 4);  // one arrive per warp of the warpgroup
+        for (int x = 0; x < kWG; ++x) mbar_init(ds_full + x, 4);
         mbar_init(dkv_full, 1);
         fence_barrier_init();
     }
@@ -297,7 +329,7 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     griddep_wait();  // inputs written by the previous kernel in the stream are visible
-    if (warp < 4) regs_dec<88>();
+    if (warp < 4) regs_dec<Cfg::kRegsLo>();
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
@@ -342,17 +374,21 @@ __global__ void __launch_bounds__(384, 1)
             for (int kk = 0; kk < kD / 16; ++kk)
                 mma_ss_e(tmem + dcol, desc_kmajor(ad, kk), desc_kmajor(bd, kk), idesc_kk, kk > 0);
         };
-        // A operand (16-bit) held in TMEM by the two warpgroups: queries
-        // [64h, 64h+64) at columns base + 64h + [0, 32).
-        // Warpgroup h's four K-steps are issued as soon as h published (`ready[h]`).
-        auto issue_ts = [&](uint32_t dcol, uint32_t abase_col, uint64_t bd, bool acc, uint64_t* ready, uint32_t ph) {
+        // A operand (16-bit) held in TMEM by the math warpgroups: queries
+        // [kQW h, kQW h + kQW) at columns base + kQW h + [0, kQW / 2).
+        // Warpgroup h's K-steps (16 queries each) are issued as soon as h published
+        // (`ready[h]`), or (kHalf) as soon as their half landed (`ready[kHv h + half]`).
+        auto issue_ts = [&](uint32_t dcol, uint32_t abase_col, uint64_t bd, bool acc, uint64_t* ready, uint32_t ph,
+                            auto half_gran) {
+            constexpr int kHalfN = decltype(half_gran)::value ? kHv : 1;  // publication chunks per warpgroup
+            constexpr int kPer = kQW / 16;                                // K-steps per warpgroup
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-                if ((kk & 3) == 0) {
-                    mbar_wait_mma(ready + (kk >> 2), ph);
+                if (kk % (kPer / kHalfN) == 0) {
+                    mbar_wait_mma(ready + (kk / kPer) * kHalfN + (kk % kPer) / (kPer / kHalfN), ph);
                     tc_fence_after();
                 }
-                mma_ts_e(tmem + dcol, tmem + abase_col + (kk >> 2) * 64 + (kk & 3) * 8, desc_mnmajor(bd, kk),
+                mma_ts_e(tmem + dcol, tmem + abase_col + (kk / kPer) * kQW + (kk % kPer) * 8, desc_mnmajor(bd, kk),
                          idesc_kmn, (acc || kk > 0) ? 1u : 0u);
             }
         };
@@ -376,8 +412,9 @@ __global__ void __launch_bounds__(384, 1)
                 const int st = s % kSt, st1 = (s + 1) % kSt, st2 = (s + 2) % kSt;
                 const uint32_t R = (s & 1) * 128u;
                 stress_delay(3, s);
-                issue_ts(Cfg::kTmemDV, Cfg::kTmemS + R, dDOm + st * kTile16, s > 0, p_full + 2 * (s & 1), (s >> 1) & 1);  // dV += P^T dO
-                issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, s & 1);      // dK += dS^T Q
+                issue_ts(Cfg::kTmemDV, Cfg::kTmemS + R, dDOm + st * kTile16, s > 0, p_full + kWG * kHv * (s & 1), (s >> 1) & 1,
+                         std::true_type{});  // dV += P^T dO
+                issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, s & 1, std::false_type{});  // dK += dS^T Q
                 mma_commit_e(q_empty + st);
                 if (s + 1 < n_steps) {
                     issue_kk(Cfg::kTmemDP, dV, dDOk + st1 * kTile16);  // after dK read dS^T
@@ -395,7 +432,8 @@ __global__ void __launch_bounds__(384, 1)
             const int st = s % kSt;
             const int st1 = (s + 1) % kSt;
             stress_delay(3, s);
-            issue_ts(Cfg::kTmemDV, Cfg::kTmemS, dDOm + st * kTile16, s > 0, p_full + 2 * (s & 1), (s >> 1) & 1);  // dV += P^T dO
+            issue_ts(Cfg::kTmemDV, Cfg::kTmemS, dDOm + st * kTile16, s > 0, p_full + kWG * kHv * (s & 1), (s >> 1) & 1,
+                     std::true_type{});  // dV += P^T dO
             VTRACE(8 * s + 0);
             if (s + 1 < n_steps) {
                 mbar_wait(q_full + st1, ((s + 1) / kSt) & 1);
@@ -404,7 +442,7 @@ __global__ void __launch_bounds__(384, 1)
                 issue_kk(Cfg::kTmemS, dK, dQk + st1 * kTile16);  // in-order after dV read P^T
                 mma_commit_e(s_full);
             }
-            issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, s & 1);  // dK += dS^T Q
+            issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, s & 1, std::false_type{});  // dK += dS^T Q
             VTRACE(8 * s + 2);
             mma_commit_e(q_empty + st);
             if (s + 1 < n_steps) {
@@ -415,56 +453,68 @@ __global__ void __launch_bounds__(384, 1)
         mma_commit_e(dkv_full);
     } else if (warp >= 4) {
         // ------------------------------------------------------ P / dS warps
-        regs_inc<208>();
-        const int h = (warp - 4) >> 2;           // query-column half
+        regs_inc<Cfg::kRegsHi>();
+        const int h = (warp - 4) >> 2;           // query-column group: [kQW h, kQW h + kQW)
         const int r = ((warp & 3) << 5) + lane;  // key row == TMEM lane
         const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const int key = kb * 128 + r;
         const bool key_ok = key < N;
         const float sc = p.scale_log2;
+        constexpr int kCh = kQW / 32;            // 32-column chunks per warpgroup
         uint64_t dbase = 0;
         if constexpr (kDrop) dbase = drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H);
         for (int s = 0; s < n_steps; ++s) {
             const int st = s % kSt;
             const int i = i0 + s;
-            const float* lse2 = sLD + st * 256 + 64 * h;
-            const float* dsum = sLD + st * 256 + 128 + 64 * h;
+            const float* lse2 = sLD + st * 256 + kQW * h;
+            const float* dsum = sLD + st * 256 + 128 + kQW * h;
             const uint32_t sR = Cfg::kTmemS + (kDB ? (s & 1) * 128u : 0u);  // S / P^T region of this tile
-            uint2 kmw = make_uint2(~0u, ~0u);
-            if (kDrop && p.drop_mask_k)  // this key row's 64 query bits, key-major copy (mha_dropmask_kernel)
-                kmw = __ldg(reinterpret_cast<const uint2*>(
-                    p.drop_mask_k + (static_cast<size_t>(bh) * p.Npad + key) * (p.Npad / 32) + i * 4 + 2 * h));
+            uint32_t kmw[kCh];  // this key row's query bits, key-major copy (mha_dropmask_kernel)
+#pragma unroll
+            for (int c = 0; c < kCh; ++c) kmw[c] = ~0u;
+            if (kDrop && p.drop_mask_k) {
+                const uint32_t* mk = p.drop_mask_k + (static_cast<size_t>(bh) * p.Npad + key) * (p.Npad / 32) + i * 4 + kCh * h;
+                if constexpr (kCh == 2) {
+                    const uint2 w = __ldg(reinterpret_cast<const uint2*>(mk));
+                    kmw[0] = w.x;
+                    kmw[kCh - 1] = w.y;
+                } else {
+                    kmw[0] = __ldg(mk);
+                }
+            }
             mbar_wait(q_full + st, (s / kSt) & 1);  // lse2 / D of this tile landed
             mbar_wait(s_full + (kDB ? (s & 1) : 0), kDB ? ((s >> 1) & 1) : (s & 1));
             tc_fence_after();
             stress_delay(1, s);
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 0);
-            float pr[64];
-            tmem_ld32f(tmem + lb + sR + 64 * h, pr);
-            tmem_ld32f(tmem + lb + sR + 64 * h + 32, pr + 32);
+            float pr[kQW];
+#pragma unroll
+            for (int c = 0; c < kCh; ++c) tmem_ld32f(tmem + lb + sR + kQW * h + 32 * c, pr + 32 * c);
             tmem_wait_ld();
-            const int qbase = i * 128 + 64 * h;
-            uint64_t keepm = ~0ull;  // dropout keep bits of this thread's 64 (query, key) positions
+            const int qbase = i * 128 + kQW * h;
+            uint64_t keepm = ~0ull;  // dropout keep bits of this thread's kQW (query, key) positions
             if (kDrop && p.drop_mask_k) {
-                keepm = static_cast<uint64_t>(kmw.x) | (static_cast<uint64_t>(kmw.y) << 32);
+                keepm = static_cast<uint64_t>(kmw[0]) | (static_cast<uint64_t>(kmw[kCh - 1]) << (kCh == 2 ? 32 : 0));
             } else if constexpr (kDrop) {
-                // row prefixes of the reference hash for this warpgroup's 64 queries
+                // row prefixes of the reference hash for this warpgroup's queries
                 named_bar_sync(1 + h, 128);  // previous step's readers are done
-                if ((warp & 3) * 32 + lane < 64)
-                    sDrop[64 * h + (warp & 3) * 32 + lane] = drop_row(dbase, qbase + (warp & 3) * 32 + lane);
+                if ((warp & 3) * 32 + lane < kQW)
+                    sDrop[kQW * h + (warp & 3) * 32 + lane] = drop_row(dbase, qbase + (warp & 3) * 32 + lane);
                 named_bar_sync(1 + h, 128);
                 keepm = 0;
 #pragma unroll 1
-                for (int x = 0; x < 64; ++x)  // (fallback without a mask: kept out of the i-cache)
-                    keepm |= static_cast<uint64_t>(drop_keep(sDrop[64 * h + x], key, p.drop_thresh)) << x;
+                for (int x = 0; x < kQW; ++x)  // (fallback without a mask: kept out of the i-cache)
+                    keepm |= static_cast<uint64_t>(drop_keep(sDrop[kQW * h + x], key, p.drop_thresh)) << x;
             }
-            // P = exp2(S c - lse2).  The two warpgroups exponentiate at the same time on
-            // the same MUFU, so VATTN_POLY_DKDV*_WG1 of every 4 element pairs of warpgroup 1
-            // go to the FMA-pipe polynomial instead (asymmetric on purpose, sm100_ptx.cuh).
-            auto p_pass = [&](auto npoly) {
+            // P = exp2(S c - lse2) of one 32-query chunk.  The warpgroups exponentiate at the
+            // same time on the same MUFU, so VATTN_POLY_DKDV*_WG1 of every 4 element pairs of
+            // the odd warpgroups go to the FMA-pipe polynomial instead (asymmetric on
+            // purpose, sm100_ptx.cuh).
+            auto p_chunk = [&](auto npoly, auto chunk) {
                 constexpr int kNP = decltype(npoly)::value;
+                constexpr int x0 = 32 * decltype(chunk)::value;
 #pragma unroll
-                for (int x = 0; x < 64; x += 4) {
+                for (int x = x0; x < x0 + 32; x += 4) {
                     const float4 l4 = *reinterpret_cast<const float4*>(lse2 + x);
                     const float2 sc2 = make_float2(sc, sc);
                     float2 a = ffma2(make_float2(pr[x], pr[x + 1]), sc2, make_float2(-l4.x, -l4.y));
@@ -477,49 +527,70 @@ __global__ void __launch_bounds__(384, 1)
                     pr[x + 2] = b.x;
                     pr[x + 3] = b.y;
                 }
-            };
-            if (h == 0)  // warp-uniform
-                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DKDV64_WG0 : VATTN_POLY_DKDV_WG0>{});
-            else
-                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DKDV64_WG1 : VATTN_POLY_DKDV_WG1>{});
-            // masks only on the (warp-uniform) diagonal tile / the last key tile
-            if ((p.causal && i == kb) || kb * 128 + 128 > N) {
-                // P = 0 for columns x < lim: key > query on the diagonal, all for keys >= N
-                const int lim = !key_ok ? 64 : ((p.causal && i == kb) ? key - qbase : 0);
+                // masks only on the (warp-uniform) diagonal tile / the last key tile:
+                // P = 0 for columns x < lim (key > query on the diagonal, all for keys >= N)
+                if ((p.causal && i == kb) || kb * 128 + 128 > N) {
+                    const int lim = !key_ok ? kQW : ((p.causal && i == kb) ? key - qbase : 0);
 #pragma unroll
-                for (int x = 0; x < 64; ++x)
-                    if (x < lim) pr[x] = 0.0f;
-            }
-            {
-                uint32_t pk[32];
+                    for (int x = x0; x < x0 + 32; ++x)
+                        if (x < lim) pr[x] = 0.0f;
+                }
+            };
+            auto pack_chunk = [&](uint32_t (&pk)[16], int x0) {
                 if constexpr (kDrop) {  // dV operand f16(P * drop) (attention_backward.cpp:163-167)
                     const float2 ik2 = make_float2(p.inv_keep, p.inv_keep);
 #pragma unroll
-                    for (int x = 0; x < 32; ++x) {
-                        const float2 pd = fmul2(make_float2(pr[2 * x], pr[2 * x + 1]), ik2);  // packed FMUL2
-                        pk[x] = pack2<kBF16>((keepm >> (2 * x)) & 1 ? pd.x : 0.0f, (keepm >> (2 * x + 1)) & 1 ? pd.y : 0.0f);
+                    for (int x = 0; x < 16; ++x) {
+                        const int e = x0 + 2 * x;
+                        const float2 pd = fmul2(make_float2(pr[e], pr[e + 1]), ik2);  // packed FMUL2
+                        pk[x] = pack2<kBF16>((keepm >> e) & 1 ? pd.x : 0.0f, (keepm >> (e + 1)) & 1 ? pd.y : 0.0f);
                     }
                 } else {
 #pragma unroll
-                    for (int x = 0; x < 32; ++x) pk[x] = pack2<kBF16>(pr[2 * x], pr[2 * x + 1]);
+                    for (int x = 0; x < 16; ++x) pk[x] = pack2<kBF16>(pr[x0 + 2 * x], pr[x0 + 2 * x + 1]);
                 }
-                tmem_st32(tmem + lb + sR + 64 * h, pk);  // own columns only
-            }
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(p_full + 2 * (s & 1) + h);
+            };
+            auto publish = [&](int half) {  // this chunk's tcgen05.st has been waited on
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full + kWG * kHv * (s & 1) + kHv * h + half);
+            };
+            // P^T chunk by chunk: chunk 0 is stored (tcgen05.st) and published while chunk 1
+            // is exponentiated.
+            auto p_pass = [&](auto npoly) {
+                uint32_t pa[16];
+                p_chunk(npoly, std::integral_constant<int, 0>{});
+                pack_chunk(pa, 0);
+                tmem_st16(tmem + lb + sR + kQW * h, pa);  // own columns only
+                if constexpr (kCh == 2) {
+                    uint32_t pb[16];
+                    p_chunk(npoly, std::integral_constant<int, 1>{});
+                    pack_chunk(pb, 32);
+                    tmem_wait_st();
+                    publish(0);
+                    tmem_st16(tmem + lb + sR + kQW * h + 16, pb);
+                    tmem_wait_st();
+                    publish(1);
+                } else {
+                    tmem_wait_st();
+                    publish(0);
+                }
+            };
+            if ((h & 1) == 0)  // warp-uniform
+                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DKDV64_WG0 : VATTN_POLY_DKDV_WG0>{});
+            else
+                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DKDV64_WG1 : VATTN_POLY_DKDV_WG1>{});
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 1);
             stress_delay(2, s);
 
             mbar_wait(dp_full, s & 1);
             tc_fence_after();
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 2);
-            uint32_t dsp[32];
+            uint32_t dsp[kQW / 2];
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
+            for (int c = 0; c < kCh; ++c) {
                 float dpv[32];
-                tmem_ld32f(tmem + lb + Cfg::kTmemDP + 64 * h + 32 * c, dpv);
+                tmem_ld32f(tmem + lb + Cfg::kTmemDP + kQW * h + 32 * c, dpv);
                 tmem_wait_ld();
 #pragma unroll
                 for (int x = 0; x < 32; x += 4) {
@@ -547,7 +618,10 @@ __global__ void __launch_bounds__(384, 1)
                     dsp[16 * c + x / 2 + 1] = pack2<kBF16>(s1.x, s1.y);
                 }
             }
-            tmem_st32(tmem + lb + Cfg::kTmemDP + 64 * h, dsp);  // dS^T over our dP^T columns
+            if constexpr (kCh == 2)
+                tmem_st32(tmem + lb + Cfg::kTmemDP + kQW * h, dsp);  // dS^T over our dP^T columns
+            else
+                tmem_st16(tmem + lb + Cfg::kTmemDP + kQW * h, dsp);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
@@ -555,22 +629,26 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_arrive(ds_full + h);
                 mbar_arrive(q_empty + st);  // done with lse2 / D of this stage
             }
-            // dS^T materialisation after publishing: dK_i starts while the tile is staged
-            const bool ds_store_thread = (warp & 3) == 0 && lane == 0;  // one per warpgroup
+            // dS^T materialisation after publishing: dK_i starts while the tile is staged.
+            // One 64-query x 128-key box per 64 queries (one or two warpgroups write it);
+            // the box's first warpgroup's first thread issues its TMA store (replaces
+            // 16-byte global stores that stalled the math warps, profiles/r2_experiments.md)
             if (p.ds_out) {
-                // dS^T tile -> swizzled smem box (this warpgroup's 64 queries x 128 keys) ->
-                // TMA store, off the critical path (replaces 16-byte global stores that
-                // stalled the dS pass)
-                uint8_t* box = smem + Cfg::kSmemDsStage + h * 16384;
+                constexpr int kBoxWG = 64 / kQW;               // warpgroups per box
+                const int bx = h / kBoxWG;                      // box (64-query group)
+                const bool ds_store_thread = (h % kBoxWG) == 0 && (warp & 3) == 0 && lane == 0;
+                const uint32_t bar_id = kBoxWG == 1 ? 1 + h : 5 + bx, bar_n = 128 * kBoxWG;
+                uint8_t* box = smem + Cfg::kSmemDsStage + bx * 16384;
                 if (ds_store_thread) bulk_wait_read0();  // the previous box left the buffer
-                named_bar_sync(1 + h, 128);
+                named_bar_sync(bar_id, bar_n);
+                const int m0 = (h % kBoxWG) * (kQW / 8);    // first 16-byte chunk of this warpgroup's row part
 #pragma unroll
-                for (int m = 0; m < 8; ++m)
-                    st_swz128(box, r, m, make_uint4(dsp[4 * m], dsp[4 * m + 1], dsp[4 * m + 2], dsp[4 * m + 3]));
+                for (int m = 0; m < kQW / 8; ++m)
+                    st_swz128(box, r, m0 + m, make_uint4(dsp[4 * m], dsp[4 * m + 1], dsp[4 * m + 2], dsp[4 * m + 3]));
                 fence_proxy_async_smem();
-                named_bar_sync(1 + h, 128);
+                named_bar_sync(bar_id, bar_n);
                 if (ds_store_thread) {
-                    tma_store_3d(&tm_ds, box, 64 * h, 0,
+                    tma_store_3d(&tm_ds, box, 64 * bx, 0,
                                  static_cast<int>(static_cast<long long>(bh) * p.ds_tiles_per_bh + ds_tile_index(p, i, kb)));
                     bulk_commit();
                 }
@@ -584,16 +662,29 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         T16* dk = reinterpret_cast<T16*>(dk_out) + (static_cast<size_t>(bh) * N + key) * kD;
         T16* dv = reinterpret_cast<T16*>(dv_out) + (static_cast<size_t>(bh) * N + key) * kD;
+        constexpr int kCols = kD / kWG;  // dK / dV columns per warpgroup (16, 32 or 64)
+        constexpr int kEc = kCols < 32 ? kCols : 32;
 #pragma unroll
-        for (int c = 0; c < kD / 64; ++c) {
-            const int col = h * (kD / 2) + 32 * c;
+        for (int c = 0; c < kCols / kEc; ++c) {
+            const int col = h * kCols + kEc * c;
             float a[32], b[32];
-            tmem_ld32f(tmem + lb + Cfg::kTmemDV + col, a);
-            tmem_ld32f(tmem + lb + Cfg::kTmemDK + col, b);
+            if constexpr (kEc == 32) {
+                tmem_ld32f(tmem + lb + Cfg::kTmemDV + col, a);
+                tmem_ld32f(tmem + lb + Cfg::kTmemDK + col, b);
+            } else {
+                uint32_t ua[16], ub[16];
+                tmem_ld16(tmem + lb + Cfg::kTmemDV + col, ua);
+                tmem_ld16(tmem + lb + Cfg::kTmemDK + col, ub);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    a[e] = __uint_as_float(ua[e]);
+                    b[e] = __uint_as_float(ub[e]);
+                }
+            }
             tmem_wait_ld();
             if (key_ok) {
 #pragma unroll
-                for (int x = 0; x < 4; ++x) {
+                for (int x = 0; x < kEc / 8; ++x) {
                     uint4 va, vb;
                     va.x = pack2<kBF16>(a[8 * x + 0], a[8 * x + 1]);
                     va.y = pack2<kBF16>(a[8 * x + 2], a[8 * x + 3]);

@@ -2,7 +2,7 @@
 # Rebuild the round-1 barrier protocol under the schedule fuzzer, for the hang
 # root-cause record: a copy of csrc/ with the two per-step-parity
 # barrier pairs folded back into one barrier each --
-#   dK/dV  p_full[s & 1][h] -> p_full[h]        (parity s & 1)
+#   dK/dV  p_full[s & 1][h][half] -> p_full[h][half]   (parity s & 1)
 #   dQ     ds_full[j & 1]   -> ds_full          (parity j & 1)
 # -> tools/variants/stress_legacy.so (load with VATTN_LIB=...).  Never shipped.
 set -e
@@ -16,8 +16,8 @@ import sys
 p = sys.argv[1]
 s = open(p).read()
 subs = [
-    ("p_full + 2 * (s & 1), (s >> 1) & 1)", "p_full, s & 1)", 2),
-    ("mbar_arrive(p_full + 2 * (s & 1) + h)", "mbar_arrive(p_full + h)", 1),
+    ("p_full + kWG * kHv * (s & 1), (s >> 1) & 1,", "p_full, s & 1,", 2),
+    ("mbar_arrive(p_full + kWG * kHv * (s & 1) + kHv * h + half)", "mbar_arrive(p_full + kHv * h + half)", 1),
     ("mbar_wait_mma(ds_full + (j & 1), (j >> 1) & 1)", "mbar_wait_mma(ds_full, j & 1)", 1),
     ("mbar_arrive(ds_full + (j & 1))", "mbar_arrive(ds_full)", 1),
 ]
