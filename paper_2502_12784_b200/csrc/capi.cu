@@ -90,7 +90,7 @@ EncodeFn encode_fn() {
 // a call needs 4-6 of them, which matters for launch-bound configs (C1, C4).
 // Direct-mapped, 256 entries, one mutex (lookups are ~100 ns).
 struct MapKey {
-    int kind;  // 0 = [BH, N, d] operand, 1 = dS^T scratch
+    int kind;  // 0 = [BH, N, d] operand, 1 = dS^T scratch, 2 = operand in 64-row boxes
     const void* ptr;
     long long a, b, c;
     bool bf16;
@@ -135,8 +135,9 @@ struct MapCache {
 MapCache g_maps;
 std::atomic<long long> g_map_hits{0}, g_map_misses{0};
 
-// [B*H, N, d] 16-bit tensor, 128 rows x 64 columns per box, 128-byte swizzle.
-bool encode_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16) {
+// [B*H, N, d] 16-bit tensor, `rows` (128, or 64 for the CTA pair's half tiles) x 64
+// columns per box, 128-byte swizzle.
+bool encode_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16, int rows = 128) {
     EncodeFn enc = encode_fn();
     if (!enc) {
         g_err = "cuTensorMapEncodeTiled: driver entry point unavailable";
@@ -146,7 +147,7 @@ bool encode_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16
                                 static_cast<cuuint64_t>(BH)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2,
                                    static_cast<cuuint64_t>(D) * 2 * static_cast<cuuint64_t>(N)};
-    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(rows), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     auto encode = [&] {
         return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
@@ -171,14 +172,14 @@ bool encode_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16
     return r == CUDA_SUCCESS;
 }
 
-bool make_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16) {
-    const MapKey k{0, ptr, BH, N, D, bf16};
+bool make_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16, int rows = 128) {
+    const MapKey k{rows == 128 ? 0 : 2, ptr, BH, N, D, bf16};
     if (g_maps.get(k, m)) {
         g_map_hits.fetch_add(1, std::memory_order_relaxed);
         return true;
     }
     g_map_misses.fetch_add(1, std::memory_order_relaxed);
-    if (!encode_map(m, ptr, BH, N, D, bf16)) return false;
+    if (!encode_map(m, ptr, BH, N, D, bf16, rows)) return false;
     g_maps.put(k, *m);
     return true;
 }
@@ -315,7 +316,7 @@ int bh_group(int BH, long long per_unit_bytes, bool fwd) {
 // otherwise start in the final wave and leave a ~60 us per-SM tail at C3).  The rest
 // stays unit-major: all key tiles of one unit share its Q/dO stream in L2 (a fully
 // grouped order measured 3 % slower per CTA).  VATTN_DKDV_TAIL_WAVES overrides (0 = off).
-int dkdv_tail_units(int BH, int n_q) {
+int dkdv_tail_units(int BH, int n_q, int ctas_per_item = 1) {
     static const double waves = [] {
         const char* e = getenv("VATTN_DKDV_TAIL_WAVES");
         return e ? atof(e) : 3.5;
@@ -328,7 +329,7 @@ int dkdv_tail_units(int BH, int n_q) {
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
         sm_count[dev].store(sms, std::memory_order_relaxed);
     }
-    const int T = static_cast<int>((waves * sms + n_q - 1) / n_q);
+    const int T = static_cast<int>((waves * (sms / ctas_per_item) + n_q - 1) / n_q);
     return T < 0 ? 0 : (T > BH ? BH : T);
 }
 
@@ -367,6 +368,28 @@ cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, int sme
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
     if (e != cudaSuccess) g_launch_err = e;  // reported by the call's final error check
+    return e;
+}
+// The same with (2,1,1) clusters (CTA pairs: cta_group::2 kernels).
+template <typename... Params, typename... Args>
+cudaError_t launch_pdl_pair(void (*kernel)(Params...), dim3 grid, dim3 block, int smem, cudaStream_t stream,
+                            Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+    if (e != cudaSuccess) g_launch_err = e;
     return e;
 }
 
@@ -535,7 +558,17 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     set_dropout(c, &p.H, &p.bh_off, &p.inv_keep, &p.drop_seed, &p.drop_thresh);
     p.ds_out = L.materialize_ds ? reinterpret_cast<uint16_t*>(w + L.ds) : nullptr;
     p.ds_tiles_per_bh = L.ds_tiles_per_bh;
-    p.tail_units = c->causal ? dkdv_tail_units(BH, L.n_q) : 0;
+    // d = 128, VATTN_DKDV_PAIR=1: CTA pairs (cta_group::2 M = 256 MMAs, half the B-operand
+    // shared-memory reads).  Off by default: measured 1-3 % slower than one CTA per key
+    // tile at C3 / C5 (DESIGN 2.2 -- the step is bound by the P pass -> dV -> S chain, which
+    // the pair does not shorten, not by shared-memory bandwidth).
+    static const bool pair_env = [] {
+        const char* e = getenv("VATTN_DKDV_PAIR");
+        return e && atoi(e) == 1;
+    }();
+    const bool pair = kD == 128 && pair_env;
+    const int n_pairs = (L.n_q + 1) / 2;
+    p.tail_units = c->causal ? (pair ? dkdv_tail_units(BH, n_pairs, 2) : dkdv_tail_units(BH, L.n_q)) : 0;
     p.drop_mask = nullptr;
     p.drop_mask_k = nullptr;
     bool mask_kernel = false;
@@ -554,15 +587,30 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     if (L.materialize_ds && !make_ds_map(&mds, p.ds_out, static_cast<long long>(BH) * L.ds_tiles_per_bh, kBF16))
         return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled (dS) failed");
     // 2) dK, dV (key-major)
-    {
+    bool dkdv_launched = false;
+    if constexpr (kD == 128) {
+      if (pair) {
+        CUtensorMap mq64, mdo64;
+        if (!make_map(&mq64, q, BH, N, kD, kBF16, 64) || !make_map(&mdo64, dout, BH, N, kD, kBF16, 64))
+            return fail(VATTN_ECUDA, g_err.empty() ? "cuTensorMapEncodeTiled failed" : g_err);
+        auto kern = mha_bwd_dkdv_kernel<kD, kBF16, kDrop, true>;
+        constexpr int smem = DkdvCfg<kD>::kSmemBytes;
+        const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop, true>>(smem);
+        if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
+        ProfScope prof(stream, 1);
+        launch_pdl_pair(kern, dim3(2 * n_pairs * BH), dim3(DkdvCfg<kD>::kThreads), smem, stream, mq, mk, mv, mdo,
+                        L.materialize_ds ? mds : mq, mq64, mdo64, dk, dv, p);
+        dkdv_launched = true;
+      }
+    }
+    if (!dkdv_launched) {
         auto kern = mha_bwd_dkdv_kernel<kD, kBF16, kDrop>;
         constexpr int smem = DkdvCfg<kD>::kSmemBytes;
         const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
         launch_pdl(kern, dim3(L.n_q * BH), dim3(DkdvCfg<kD>::kThreads), smem, stream, mq, mk, mv, mdo,
-                   L.materialize_ds ? mds : mq, dk, dv,
-                   p);
+                   L.materialize_ds ? mds : mq, mq, mdo, dk, dv, p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)
     if (L.materialize_ds) {

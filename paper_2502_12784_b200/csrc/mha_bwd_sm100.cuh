@@ -248,23 +248,39 @@ struct DkdvCfg {
     // bits are hashed in place (no keep-bit mask) -- and then materialisation is off.
     static constexpr int kSmemDsStage = kSmemDrop;
     static constexpr int kSmemBar = kSmemDsStage + 32768;
-    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 1 + 2 * kWG * kHalves + kWG + 1;
+    // kv_full, q_full/q_empty [kStages], s_full (x2 double S), dp_full, p_full, ds_full,
+    // dkv_full, ld_full [kStages] (CTA pair: lse2 / D of this CTA; Q / dO count on the
+    // leader's q_full)
+    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 1 + 2 * kWG * kHalves + kWG + 1 + kStages;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr uint32_t kTmemS = 0;                       // region r at 128 r
     static constexpr uint32_t kTmemDP = kDoubleS ? 256 : 128;
     static constexpr uint32_t kTmemDV = kTmemDP + 128, kTmemDK = kTmemDV + kD;
 };
 
-template <int kD, bool kBF16, bool kDrop>
+// kPair (d = 128): a (2,1,1) cluster = two adjacent key tiles of one unit sharing
+// every query tile.  All four GEMMs run as cta_group::2 M = 256 MMAs issued by the
+// leader: each CTA's A rows (K, V, P^T, dS^T) stay its own, and each CTA supplies half
+// of the B operand, so the per-SM shared-memory operand reads per step fall from 192
+// to 128 KiB (the SS GEMMs at N = 128 saturate the 128 B/clk shared-memory port,
+// profiles/r2_experiments.md).  B halves must sit at the same offset in both CTAs:
+// a Q / dO stage holds [queries 0..127 x d-half r] (16 KB, the MN-major B of dK / dV)
+// and [queries 64r..64r+63 x d 0..127] (2 x 8 KB, the K-major B of S^T / dP^T).
+// The math warps are unchanged (thread = key row of their own CTA); their P^T / dS^T
+// publications arrive on the leader's barriers.
+template <int kD, bool kBF16, bool kDrop, bool kPair = false>
 __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
     mha_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v,
                         const __grid_constant__ CUtensorMap tm_do,
-                        const __grid_constant__ CUtensorMap tm_ds, void* __restrict__ dk_out,
-                        void* __restrict__ dv_out, const BwdParams p) {
+                        const __grid_constant__ CUtensorMap tm_ds,
+                        const __grid_constant__ CUtensorMap tm_q64,   // 64-row boxes (kPair)
+                        const __grid_constant__ CUtensorMap tm_do64,  // 64-row boxes (kPair)
+                        void* __restrict__ dk_out, void* __restrict__ dv_out, const BwdParams p) {
     VCTA(1, 0);
     using Cfg = DkdvCfg<kD>;
+    static_assert(!kPair || (kD == 128 && !Cfg::kDoubleS), "CTA pair: d = 128 only");
     constexpr int kVtraceKid = 1;
     (void)kVtraceKid;
     using T16 = typename std::conditional<kBF16, __nv_bfloat16, __half>::type;
@@ -297,16 +313,36 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
     uint64_t* p_full = dp_full + 1;              // [2][warpgroup][half]
     uint64_t* ds_full = p_full + 2 * kWG * kHv;  // [warpgroup]
     uint64_t* dkv_full = ds_full + kWG;
+    // lse2 / D of a stage: the CTA pair's own barrier (its Q / dO bytes count on the
+    // leader's q_full); one CTA: part of q_full
+    uint64_t* ld_full = kPair ? dkv_full + 1 : q_full;  // [kSt]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
     const int warp = warp_id();
     const int lane = lane_id();
+    const uint32_t rank = kPair ? cluster_rank() : 0u;  // 0 = leader (issues the MMAs)
     // causal: the key tiles with the most query tiles first
     int bh, kb;
-    grid_item_tail(p.n_q, p.tail_units, bh, kb);
+    if constexpr (kPair) {  // cluster c = key tiles (2 pr, 2 pr + 1) of unit bh
+        int pr;
+        grid_item_tail_n(static_cast<int>(blockIdx.x >> 1), static_cast<int>(gridDim.x >> 1), (p.n_q + 1) >> 1,
+                         p.tail_units, bh, pr);
+        kb = 2 * pr + static_cast<int>(rank);
+    } else {
+        grid_item_tail(p.n_q, p.tail_units, bh, kb);
+    }
     const int N = p.N;
-    const int i0 = p.causal ? kb : 0;
+    // causal: both CTAs of a pair start at the lower key tile's diagonal (the upper
+    // tile's first query tile is fully masked)
+    const int i0 = p.causal ? (kPair ? (kb & ~1) : kb) : 0;
     const int n_steps = p.n_q - i0;
+    // a math warp's arrival on a barrier the MMA issuer waits on (the leader's for a pair)
+    auto arrive_mma = [&](uint64_t* bar) {
+        if constexpr (kPair)
+            mbar_arrive_cluster(mapa_u32(bar, 0));
+        else
+            mbar_arrive(bar);
+    };
 
     if (threadIdx.x == 0) {
         if ((smem_u32(smem) & 1023u) != 0) __trap();
@@ -318,14 +354,23 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
         mbar_init(s_full, 1);
         if (kDB) mbar_init(s_full + 1, 1);
         mbar_init(dp_full, 1);
-        for (int x = 0; x < 2 * kWG * kHv; ++x) mbar_init(p_full + x, 4);  // one arrive per warp of the warpgroup
-        for (int x = 0; x < kWG; ++x) mbar_init(ds_full + x, 4);
+        // one arrive per warp of the warpgroup (of both CTAs for a pair)
+        for (int x = 0; x < 2 * kWG * kHv; ++x) mbar_init(p_full + x, kPair ? 8 : 4);
+        for (int x = 0; x < kWG; ++x) mbar_init(ds_full + x, kPair ? 8 : 4);
         mbar_init(dkv_full, 1);
+        if (kPair)
+            for (int s = 0; s < kSt; ++s) mbar_init(ld_full + s, 1);
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<512>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair) {
+        if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
+        tc_fence_before();
+        cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
+    } else {
+        if (warp == 2) tmem_alloc<512>(tmem_slot);
+        tc_fence_before();
+        __syncthreads();
+    }
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     griddep_wait();  // inputs written by the previous kernel in the stream are visible
@@ -338,41 +383,87 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
             tma_prefetch_desc(&tm_do);
-            mbar_arrive_expect_tx(kv_full, 2 * Cfg::kTileBytes);
-            for (int b = 0; b < Cfg::kBoxes; ++b) {
-                tma_load_3d(sK + b * 16384, &tm_k, kv_full, b * 64, kb * 128, bh);
-                tma_load_3d(sV + b * 16384, &tm_v, kv_full, b * 64, kb * 128, bh);
+            if constexpr (kPair) {
+                tma_prefetch_desc(&tm_q64);
+                tma_prefetch_desc(&tm_do64);
+                // K, V of both CTAs count on the leader's kv_full
+                const uint32_t kv_cl = mapa_u32(kv_full, 0);
+                if (rank == 0) mbar_arrive_expect_tx(kv_full, 4 * Cfg::kTileBytes);
+                for (int b = 0; b < Cfg::kBoxes; ++b) {
+                    tma_load_3d_pair(sK + b * 16384, &tm_k, kv_cl, b * 64, kb * 128, bh);
+                    tma_load_3d_pair(sV + b * 16384, &tm_v, kv_cl, b * 64, kb * 128, bh);
+                }
+            } else {
+                mbar_arrive_expect_tx(kv_full, 2 * Cfg::kTileBytes);
+                for (int b = 0; b < Cfg::kBoxes; ++b) {
+                    tma_load_3d(sK + b * 16384, &tm_k, kv_full, b * 64, kb * 128, bh);
+                    tma_load_3d(sV + b * 16384, &tm_v, kv_full, b * 64, kb * 128, bh);
+                }
             }
             for (int s = 0; s < n_steps; ++s) {
                 const int st = s % kSt;
                 const int i = i0 + s;
                 stress_delay(4, s);
                 mbar_wait(q_empty + st, ((s / kSt) & 1) ^ 1);
-                mbar_arrive_expect_tx(q_full + st, 2 * Cfg::kTileBytes + 1024);
-                for (int b = 0; b < Cfg::kBoxes; ++b) {
-                    tma_load_3d(sQ + st * Cfg::kTileBytes + b * 16384, &tm_q, q_full + st, b * 64, i * 128, bh);
-                    tma_load_3d(sDO + st * Cfg::kTileBytes + b * 16384, &tm_do, q_full + st, b * 64, i * 128, bh);
+                uint8_t* q_st = sQ + st * Cfg::kTileBytes;
+                uint8_t* do_st = sDO + st * Cfg::kTileBytes;
+                if constexpr (kPair) {
+                    // [all 128 queries x d-half r] then [queries 64r.. +64 x d 0..127] (2 boxes)
+                    const uint32_t q_cl = mapa_u32(q_full + st, 0);
+                    if (rank == 0) mbar_arrive_expect_tx(q_full + st, 4 * Cfg::kTileBytes);
+                    const int r64 = static_cast<int>(rank) * 64;
+                    tma_load_3d_pair(q_st, &tm_q, q_cl, r64, i * 128, bh);
+                    tma_load_3d_pair(do_st, &tm_do, q_cl, r64, i * 128, bh);
+                    for (int b = 0; b < 2; ++b) {
+                        tma_load_3d_pair(q_st + 16384 + b * 8192, &tm_q64, q_cl, b * 64, i * 128 + r64, bh);
+                        tma_load_3d_pair(do_st + 16384 + b * 8192, &tm_do64, q_cl, b * 64, i * 128 + r64, bh);
+                    }
+                    mbar_arrive_expect_tx(ld_full + st, 1024);
+                } else {
+                    mbar_arrive_expect_tx(q_full + st, 2 * Cfg::kTileBytes + 1024);
+                    for (int b = 0; b < Cfg::kBoxes; ++b) {
+                        tma_load_3d(q_st + b * 16384, &tm_q, q_full + st, b * 64, i * 128, bh);
+                        tma_load_3d(do_st + b * 16384, &tm_do, q_full + st, b * 64, i * 128, bh);
+                    }
                 }
                 const size_t ro = static_cast<size_t>(bh) * p.Npad + static_cast<size_t>(i) * 128;
-                bulk_load(sLD + st * 256, p.lse2 + ro, 512, q_full + st);
-                bulk_load(sLD + st * 256 + 128, p.dsum + ro, 512, q_full + st);
+                bulk_load(sLD + st * 256, p.lse2 + ro, 512, ld_full + st);
+                bulk_load(sLD + st * 256 + 128, p.dsum + ro, 512, ld_full + st);
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 && (!kPair || rank == 0)) {
         // ------------------------------------------------ MMA issuer (whole warp)
-        constexpr uint32_t idesc_kk = umma_idesc_f16(128, 128, kBF16, 0, 0);  // S^T, dP^T
-        constexpr uint32_t idesc_kmn = umma_idesc_f16(128, kD, kBF16, 0, 1);  // dV, dK
+        constexpr uint32_t kM = kPair ? 256 : 128;
+        constexpr uint32_t idesc_kk = umma_idesc_f16(kM, 128, kBF16, 0, 0);  // S^T, dP^T
+        constexpr uint32_t idesc_kmn = umma_idesc_f16(kM, kD, kBF16, 0, 1);  // dV, dK
         constexpr uint64_t kTile16 = Cfg::kTileBytes >> 4;
+        constexpr int kHalfB = kPair ? 16384 : 0;  // pair: the K-major 64-query half follows the MN-major d-half
         const uint64_t dK = umma_desc_sw128(smem_u32(sK), 16, 1024);
         const uint64_t dV = umma_desc_sw128(smem_u32(sV), 16, 1024);
-        const uint64_t dQk = umma_desc_sw128(smem_u32(sQ), 16, 1024);       // Q as K-major B
-        const uint64_t dDOk = umma_desc_sw128(smem_u32(sDO), 16, 1024);     // dO as K-major B
+        const uint64_t dQk = umma_desc_sw128(smem_u32(sQ + kHalfB), 16, 1024);    // Q as K-major B
+        const uint64_t dDOk = umma_desc_sw128(smem_u32(sDO + kHalfB), 16, 1024);  // dO as K-major B
         const uint64_t dQm = umma_desc_sw128(smem_u32(sQ), 16384, 1024);    // Q as MN-major B
         const uint64_t dDOm = umma_desc_sw128(smem_u32(sDO), 16384, 1024);  // dO as MN-major B
+        auto mma_commit_e = [&](uint64_t* bar) {  // a pair's commit arrives in both CTAs
+            if constexpr (kPair)
+                mma_commit_pair(bar);
+            else
+                vattn_sm100::mma_commit_e(bar);
+        };
+        auto mbar_wait_mma = [&](uint64_t* bar, uint32_t ph) {  // the peer's warps arrive here too
+            if constexpr (kPair)
+                mbar_wait_mma_cl(bar, ph);
+            else
+                vattn_sm100::mbar_wait_mma(bar, ph);
+        };
         auto issue_kk = [&](uint32_t dcol, uint64_t ad, uint64_t bd) {
 #pragma unroll
-            for (int kk = 0; kk < kD / 16; ++kk)
-                mma_ss_e(tmem + dcol, desc_kmajor(ad, kk), desc_kmajor(bd, kk), idesc_kk, kk > 0);
+            for (int kk = 0; kk < kD / 16; ++kk) {
+                if constexpr (kPair)
+                    mma_ss_pair(tmem + dcol, desc_kmajor(ad, kk), desc_kmajor_half(bd, kk), idesc_kk, kk > 0);
+                else
+                    mma_ss_e(tmem + dcol, desc_kmajor(ad, kk), desc_kmajor(bd, kk), idesc_kk, kk > 0);
+            }
         };
         // A operand (16-bit) held in TMEM by the math warpgroups: queries
         // [kQW h, kQW h + kQW) at columns base + kQW h + [0, kQW / 2).
@@ -388,8 +479,11 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                     mbar_wait_mma(ready + (kk / kPer) * kHalfN + (kk % kPer) / (kPer / kHalfN), ph);
                     tc_fence_after();
                 }
-                mma_ts_e(tmem + dcol, tmem + abase_col + (kk / kPer) * kQW + (kk % kPer) * 8, desc_mnmajor(bd, kk),
-                         idesc_kmn, (acc || kk > 0) ? 1u : 0u);
+                const uint32_t a_col = tmem + abase_col + (kk / kPer) * kQW + (kk % kPer) * 8;
+                if constexpr (kPair)
+                    mma_ts_pair(tmem + dcol, a_col, desc_mnmajor(bd, kk), idesc_kmn, (acc || kk > 0) ? 1u : 0u);
+                else
+                    mma_ts_e(tmem + dcol, a_col, desc_mnmajor(bd, kk), idesc_kmn, (acc || kk > 0) ? 1u : 0u);
             }
         };
         mbar_wait(kv_full, 0);
@@ -482,7 +576,7 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                     kmw[0] = __ldg(mk);
                 }
             }
-            mbar_wait(q_full + st, (s / kSt) & 1);  // lse2 / D of this tile landed
+            mbar_wait(ld_full + st, (s / kSt) & 1);  // lse2 / D of this tile landed
             mbar_wait(s_full + (kDB ? (s & 1) : 0), kDB ? ((s >> 1) & 1) : (s & 1));
             tc_fence_after();
             stress_delay(1, s);
@@ -528,9 +622,10 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                     pr[x + 3] = b.y;
                 }
                 // masks only on the (warp-uniform) diagonal tile / the last key tile:
-                // P = 0 for columns x < lim (key > query on the diagonal, all for keys >= N)
-                if ((p.causal && i == kb) || kb * 128 + 128 > N) {
-                    const int lim = !key_ok ? kQW : ((p.causal && i == kb) ? key - qbase : 0);
+                // P = 0 for columns x < lim (key > query on the diagonal, all for keys >= N;
+                // a pair's upper CTA also sees the tile below its diagonal: all masked)
+                if ((p.causal && i <= kb) || kb * 128 + 128 > N) {
+                    const int lim = !key_ok ? kQW : ((p.causal && i <= kb) ? key - qbase : 0);
 #pragma unroll
                     for (int x = x0; x < x0 + 32; ++x)
                         if (x < lim) pr[x] = 0.0f;
@@ -553,7 +648,7 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             auto publish = [&](int half) {  // this chunk's tcgen05.st has been waited on
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(p_full + kWG * kHv * (s & 1) + kHv * h + half);
+                if (lane == 0) arrive_mma(p_full + kWG * kHv * (s & 1) + kHv * h + half);
             };
             // P^T chunk by chunk: chunk 0 is stored (tcgen05.st) and published while chunk 1
             // is exponentiated.
@@ -626,14 +721,15 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(ds_full + h);
+                arrive_mma(ds_full + h);
                 mbar_arrive(q_empty + st);  // done with lse2 / D of this stage
             }
             // dS^T materialisation after publishing: dK_i starts while the tile is staged.
             // One 64-query x 128-key box per 64 queries (one or two warpgroups write it);
             // the box's first warpgroup's first thread issues its TMA store (replaces
             // 16-byte global stores that stalled the math warps, profiles/r2_experiments.md)
-            if (p.ds_out) {
+            // (a pair's tiles above the diagonal or past the last key tile hold no dS)
+            if (p.ds_out && !(kPair && (kb >= p.n_q || (p.causal && kb > i)))) {
                 constexpr int kBoxWG = 64 / kQW;               // warpgroups per box
                 const int bx = h / kBoxWG;                      // box (64-query group)
                 const bool ds_store_thread = (h % kBoxWG) == 0 && (warp & 3) == 0 && lane == 0;
@@ -702,10 +798,18 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
     }
     griddep_launch_dependents();
     tc_fence_before();
-    __syncthreads();
-    if (warp == 2) {
-        tc_fence_after();
-        tmem_dealloc<512>(tmem);
+    if constexpr (kPair) {
+        cluster_sync_all();  // the leader's MMAs read the peer's smem / TMEM until dkv_full
+        if (warp == 2) {
+            tc_fence_after();
+            tmem_dealloc_pair<512>(tmem);
+        }
+    } else {
+        __syncthreads();
+        if (warp == 2) {
+            tc_fence_after();
+            tmem_dealloc<512>(tmem);
+        }
     }
     VCTA(1, 1);
 }

@@ -42,6 +42,19 @@ inline dim3 tile_grid(int ntiles, int bh, int G) { return dim3(ntiles * G, bh / 
 // 1-D variant with a longest-first tail: units [0, BH - T) unit-major, then the last T
 // units tile-major, so the heaviest causal items of the final units start waves before
 // the end instead of in the last wave (grid = ntiles * BH blocks along x).
+// Item L of `total` (= BH * ntiles) items: the same order (CTA pairs: item = cluster).
+VATTN_DEV void grid_item_tail_n(int L, int total, int ntiles, int T, int& bh, int& tile) {
+    const int BH = total / ntiles;
+    const int head = (BH - T) * ntiles;
+    if (L < head) {
+        bh = L / ntiles;
+        tile = L % ntiles;
+    } else {
+        const int r = L - head;
+        tile = r / T;
+        bh = BH - T + r % T;
+    }
+}
 VATTN_DEV void grid_item_tail(int ntiles, int T, int& bh, int& tile) {
     const int BH = static_cast<int>(gridDim.x) / ntiles;
     const int L = static_cast<int>(blockIdx.x);
@@ -366,12 +379,136 @@ VATTN_DEV void mma_commit_e(uint64_t* bar) {
         : "memory");
 }
 
+// ------------------------------------------------------------ CTA pair --
+// cta_group::2: two CTAs of a (2,1,1) cluster on one TPC run M = 256 MMAs.  The
+// leader (rank 0) issues every MMA; each CTA supplies its 128 A rows and half of the
+// B columns from its own shared memory at the same offsets, and holds its 128 rows
+// of D in its own tensor memory at the same column addresses.  Every tcgen05
+// instruction of such a kernel uses cta_group::2.
+
+VATTN_DEV uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of `p` (a shared::cta pointer) in CTA `rank` of the cluster.
+VATTN_DEV uint32_t mapa_u32(const void* p, uint32_t rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+    return a;
+}
+VATTN_DEV void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Arrive on an mbarrier given by its shared::cluster address.  Relaxed: what it
+// publishes is tensor memory (ordered by tcgen05.wait::st + tcgen05.fence::
+// before_thread_sync), and a release.cluster arrive compiles to a MEMBAR that
+// stalled the math warps (ncu: membar the top stall reason, the pair kernel 40 %
+// slower than one CTA).
+VATTN_DEV void mbar_arrive_cluster(uint32_t cl_addr) {
+#ifdef VATTN_PAIR_ACQ_CLUSTER
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+#else
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+#endif
+}
+VATTN_DEV void mbar_arrive_expect_tx_cluster(uint32_t cl_addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cl_addr), "r"(bytes)
+                 : "memory");
+}
+// Whole-warp wait for barriers the peer CTA arrives on.  Polled with the CTA-scope
+// try_wait (an acquire.cluster poll loop measured 2-3x slower MMAs and math passes on
+// the whole SM); the peer's arrivals are release.cluster after tcgen05.wait::st, and the
+// waiter's tcgen05.fence::after_thread_sync orders its MMAs after them.
+VATTN_DEV bool mbar_try_wait_cl(uint64_t* bar, uint32_t parity) {
+#ifdef VATTN_PAIR_ACQ_CLUSTER
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+#else
+    return mbar_try_wait(bar, parity);
+#endif
+}
+VATTN_DEV void mbar_wait_mma_cl(uint64_t* bar, uint32_t parity) {
+    if (!mbar_try_wait_cl(bar, parity)) {
+        const uint64_t t0 = globaltimer_ns();
+        uint32_t n = 0;
+        while (!mbar_try_wait_cl(bar, parity))
+            if ((++n & 255u) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) {
+#ifdef VATTN_WATCHDOG_PRINT
+                printf("vattn watchdog (MMA, cluster): block %d stuck on mbarrier smem+0x%x parity %u\n", (int)blockIdx.x,
+                       smem_u32(bar), parity);
+#endif
+                __trap();
+            }
+    }
+    __syncwarp();
+}
+// TMA load into this CTA's shared memory whose completion is counted on an mbarrier
+// of the pair's leader (`bar_cl`: shared::cluster address).
+VATTN_DEV void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cl, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cl)
+        : "memory");
+}
+template <uint32_t kCols>
+VATTN_DEV void tmem_alloc_pair(uint32_t* smem_dst) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)), "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols>
+VATTN_DEV void tmem_dealloc_pair(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
+}
+VATTN_DEV void mma_ss_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+VATTN_DEV void mma_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Arrive on `bar` (same shared-memory offset) in both CTAs of the pair once every
+// previously issued tcgen05.mma of this thread completes.
+VATTN_DEV void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
 // Descriptor of the kk-th K=16 slice of a 128-row SW128 operand tile whose base
 // descriptor is `d0` (address field counts 16-byte units; no carry possible
 // below 256 KB of shared memory).
 //  K-major  (rows = M/N, 64 K-elements per 128-B row, 16 KB per 64-col box)
 VATTN_DEV uint64_t desc_kmajor(uint64_t d0, int kk) {
     return d0 + static_cast<uint64_t>(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+}
+//  K-major with 64-row boxes (8 KB per 64-col box): the CTA pair's half B operand
+VATTN_DEV uint64_t desc_kmajor_half(uint64_t d0, int kk) {
+    return d0 + static_cast<uint64_t>(((kk >> 2) * 8192 + (kk & 3) * 32) >> 4);
 }
 //  MN-major (rows = K, 16 K-rows = 2048 B per slice)
 VATTN_DEV uint64_t desc_mnmajor(uint64_t d0, int kk) { return d0 + static_cast<uint64_t>((kk * 2048) >> 4); }

@@ -319,6 +319,54 @@ def test_dq_modes_vs_binary64(mode):
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+# ------------------------------------------- dK/dV on CTA pairs (cta_group::2) --
+_PAIR_CHILD = r'''
+import os, sys
+sys.path.insert(0, os.environ["ROOT"])
+import torch
+import paper_2502_12784_b200 as vb
+from oracle import pyoracle as po
+from tests.gpu_util import check_close, widen, workload
+out = {}
+# odd / even key-tile counts (a pair's upper CTA past the last tile), ragged N, the
+# diagonal of both CTAs, dropout through the keep-bit mask
+for (B, H, N, d, causal, dtype, p) in [(1, 2, 384, 128, True, torch.bfloat16, 0.0), (2, 1, 260, 128, False, torch.float16, 0.0),
+                                       (1, 1, 128, 128, True, torch.float16, 0.0), (1, 2, 1000, 128, True, torch.bfloat16, 0.0),
+                                       (1, 1, 512, 128, False, torch.bfloat16, 0.0), (1, 2, 300, 128, True, torch.float16, 0.2)]:
+    q, k, v, do = workload(29 + N, (B, H, N, d), dtype)
+    o, lse = vb.mha_forward(q, k, v, causal, dropout_p=p, seed=7)
+    dq, dk, dv = vb.mha_backward(q, k, v, o, do, lse, causal, dropout_p=p, seed=7)
+    if p == 0.0:
+        rdq, rdk, rdv = po.attention_grad_ref(widen(q), widen(k), widen(v), widen(do), causal)
+        for name, t, r in (("dQ", dq, rdq), ("dK", dk, rdk), ("dV", dv, rdv)):
+            check_close(widen(t), r, dtype, name + " pair " + os.environ["VATTN_DKDV_PAIR"])
+    a = vb.mha_backward(q, k, v, o, do, lse, causal, dropout_p=p, seed=7)
+    assert all(torch.equal(x, y) for x, y in zip((dq, dk, dv), a)), "not deterministic"
+    out[(B, H, N, causal, p)] = [t.cpu() for t in (dq, dk, dv)]
+torch.save(out, os.environ["OUT"])
+print("OK")
+'''
+
+
+def test_dkdv_cta_pair_vs_single(tmp_path):
+    """The cta_group::2 dK/dV kernel (VATTN_DKDV_PAIR=1: M = 256 MMAs over two key tiles,
+    each CTA supplying half of every B operand) meets the binary64 tolerances, is
+    deterministic, and reproduces the one-CTA kernel bit for bit (same K-step order)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for pair in ("0", "1"):
+        path = str(tmp_path / f"pair{pair}.pt")
+        r = subprocess.run([sys.executable, "-c", _PAIR_CHILD], capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, VATTN_DKDV_PAIR=pair, ROOT=root, OUT=path))
+        assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+        res[pair] = torch.load(path)
+    for key, single in res["0"].items():
+        for name, a, b in zip(("dQ", "dK", "dV"), single, res["1"][key]):
+            assert torch.equal(a, b), f"{key} {name}: pair differs from one CTA"
+
+
 # --------------------------------------- compute_dpsum and the mask digest --
 
 @pytest.mark.parametrize("d,dtype", [(64, torch.float16), (128, torch.bfloat16)])

@@ -52,6 +52,51 @@ __global__ void __launch_bounds__(128, 1) mma_bench(long long* out, int reps) {
     if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+// cta_group::2 (M = 256) throughput: the leader of each (2,1,1) cluster issues
+// reps x 8 K16 steps; each CTA supplies its A rows and half of B at the same offsets.
+template <int kN, bool kTS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mma_bench_pair(long long* out, int reps) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x / 32;
+    const uint32_t rank = cluster_rank();
+    for (int i = threadIdx.x; i < 131072 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem_alloc_pair<512>(&tslot);
+    fence_proxy_async_smem();
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (rank == 0 && warp == 0) {
+        constexpr uint32_t idesc = umma_idesc_f16(256, kN, 0, 0, 0);
+        const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+        const long long t0 = clock64();
+        for (int r = 0; r < reps; ++r) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                if (kTS)
+                    mma_ts_pair(tmem + 256, tmem + kk * 8, umma_desc_sw128(b + (kk & 3) * 32 + (kk / 4) * 32768, 16, 1024), idesc, 1);
+                else
+                    mma_ss_pair(tmem + 256, umma_desc_sw128(a + (kk & 3) * 32 + (kk / 4) * 16384, 16, 1024),
+                                umma_desc_sw128(b + (kk & 3) * 32 + (kk / 4) * 32768, 16, 1024), idesc, 1);
+            }
+        }
+        mma_commit_pair(&bar);
+        mbar_wait(&bar, 0);
+        out[blockIdx.x] = out[blockIdx.x + 1] = clock64() - t0;
+    } else if (rank == 1 && warp == 0) {
+        mbar_wait(&bar, 0);
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 0) tmem_dealloc_pair<512>(tmem);
+}
+
 __global__ void __launch_bounds__(128, 1) ldtm_bench(long long* out, int reps) {
     __shared__ uint32_t tslot;
     const int warp = threadIdx.x / 32;
@@ -166,6 +211,11 @@ int main(int argc, char** argv) {
     if (which == 3) report("TS N=64", run(mma_bench<64, true>, 148, 128, 131072, reps), 64);
     if (which == 4) report("TS N=128", run(mma_bench<128, true>, 148, 128, 131072, reps), 128);
     if (which == 5) report("TS N=256", run(mma_bench<256, true>, 148, 128, 131072, reps), 256);
+    // pair: per-SM flop/clk (each SM holds 128 of the 256 rows)
+    if (which == 10) report("pair SS N=128", run(mma_bench_pair<128, false>, 148, 128, 131072, reps) , 128);
+    if (which == 11) report("pair SS N=256", run(mma_bench_pair<256, false>, 148, 128, 131072, reps), 256);
+    if (which == 12) report("pair TS N=128", run(mma_bench_pair<128, true>, 148, 128, 131072, reps), 128);
+    if (which == 13) report("pair SS N=64", run(mma_bench_pair<64, false>, 148, 128, 131072, reps), 64);
     if (which == 7) {
         for (int threads : {128, 256, 512}) {
             long long* d;
