@@ -19,6 +19,12 @@
 // P_t (16-bit, two per column) overwrites the first 64 columns of S_t.
 // The MMA issue order S0(j+1) right after PV0(j), S1(j+1) right after PV1(j)
 // keeps the tensor pipe busy while the other tile's softmax runs.
+// Option (VATTN_FWD_SEPP=1, d = 64 only -- O needs only 128 columns): P_t lives in its
+// own region [384 + 64t, +64), so S_t(j+1) is issued as soon as the softmax has read
+// S_t(j) into registers (s_free) and the softmax warpgroups never wait for S (issue
+// order S0(j+1), S1(j+1), PV0(j), PV1(j)).  Measured (profiles/r2_experiments.md): the
+// two warpgroups then run in lock step on the shared MUFU and the step period stays
+// ~3500 clk -- C4 forward +4 %, C2 N >= 1k -4..-9 % -- so it is off.
 // O is rescaled lazily: only when a row maximum grows by more than 2^8.
 #pragma once
 
@@ -58,15 +64,45 @@ struct FwdCfg {
     static constexpr int kStages = kD == 128 ? VATTN_FWD_STAGES128 : 8;   // K/V ring depth
     static constexpr int kSmemQ = 0;                    // Q0, Q1
     static constexpr int kSmemKV = 2 * kTileBytes;
-    static constexpr int kSmemBar = kSmemKV + kStages * kTileBytes;
-    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 8 + 2;
+    // Softmax warpgroups per Q tile (VATTN_FWD_HALVES): 1 = one warpgroup per tile owns
+    // whole rows (default); 2 = each owns 64 of the 128 key columns of its rows (four
+    // softmax warpgroups, 640 threads), the row max / sum exchanged through shared
+    // memory.  Measured 1.2-2.7x slower (register cap 104 at 640 threads -- 112 deadlocks
+    // setmaxnreg.inc, the launch allocation is 640 x 96 -- spills at d = 128, and a
+    // 256-thread barrier per step), profiles/r2_experiments.md.
+#ifndef VATTN_FWD_HALVES
+#define VATTN_FWD_HALVES 1
+#endif
+    static constexpr int kHalves = VATTN_FWD_HALVES;
+    static constexpr int kSmemX = kSmemKV + kStages * kTileBytes;  // [3 slots][2 tiles][kHalves][128] f32
+    static constexpr int kSmemBar = kSmemX + 3 * 2 * kHalves * 128 * 4;
+    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 8 + 2 + 2;  // ..., o_done[2], s_free[2]
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
-    static constexpr int kThreads = 384;
+    // Warps: producer 0, MMA 1, TMEM allocator 2, idle 3, softmax warpgroups from warp 4.
+    // setmaxnreg split of the CTA's launch allocation: 88 / 208 (384 threads x 168) or,
+    // two halves (640 threads x 96), VATTN_FWD_REGS_LO / VATTN_FWD_REGS_HI.
+#ifndef VATTN_FWD_REGS_LO
+#define VATTN_FWD_REGS_LO 56
+#endif
+    static constexpr int kMathWarp0 = 4;
+    static constexpr int kAllocWarp = 2;
+    static constexpr int kThreads = 128 + 256 * kHalves;
+    static constexpr uint32_t kRegsLo = kHalves == 1 ? 88 : VATTN_FWD_REGS_LO;
+#ifndef VATTN_FWD_REGS_HI
+#define VATTN_FWD_REGS_HI 104
+#endif
+    static constexpr uint32_t kRegsHi = kHalves == 1 ? 208 : VATTN_FWD_REGS_HI;
+    static_assert(128 * kRegsLo + 256 * kHalves * kRegsHi <= 65536, "register split");
     static constexpr uint32_t kTmemO = 256;
+#ifndef VATTN_FWD_SEPP
+#define VATTN_FWD_SEPP 0
+#endif
+    static constexpr bool kSepP = kD == 64 && VATTN_FWD_SEPP;  // P in its own region (see above)
+    static constexpr uint32_t kTmemP = 384;          // kSepP: P_t at [384 + 64t, +64)
 };
 
 template <int kD, bool kBF16, bool kDrop>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
     mha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v,
@@ -79,6 +115,7 @@ __global__ void __launch_bounds__(384, 1)
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem + Cfg::kSmemQ;
     uint8_t* sKV = smem + Cfg::kSmemKV;
+    float* sX = reinterpret_cast<float*>(smem + Cfg::kSmemX);  // row max / sum exchange between column halves
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kSmemBar);
     uint64_t* q_full = bars;
     uint64_t* kv_full = bars + 1;
@@ -86,6 +123,8 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* s_full = kv_empty + S;
     uint64_t* p_full = s_full + 2;
     uint64_t* o_done = p_full + 8;  // p_full: [tile][quarter]
+    uint64_t* s_free = o_done + 2;  // kSepP: the softmax has S_t(j) in registers
+    constexpr bool kSepP = Cfg::kSepP;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
     const int warp = warp_id();
@@ -115,18 +154,19 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(s_full + t, 1);
             for (int qq = 0; qq < 4; ++qq) mbar_init(p_full + 4 * t + qq, 4);  // one arrive per warp
             mbar_init(o_done + t, 1);
+            mbar_init(s_free + t, 4 * Cfg::kHalves);  // one arrive per warp of the tile
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    if (warp == Cfg::kAllocWarp) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     griddep_wait();  // inputs written by the previous kernel in the stream are visible
-    // registers: producer/MMA warpgroup 88, softmax warpgroups 208 (384 x 168 budget);
-    // each role lowers/raises its own budget inside its branch.
-    if (warp < 4) regs_dec<88>();
+    // registers (one warpgroup per tile): producer/MMA warpgroup 88, softmax warpgroups
+    // 208 (384 x 168 budget); each role lowers/raises its own budget inside its branch.
+    if (warp < 4) regs_dec<Cfg::kRegsLo>();
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
@@ -188,7 +228,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int k2 = 0; k2 < 2; ++k2) {
                     const int kk = 2 * qq + k2;
-                    mma_ts_e(tmem + Cfg::kTmemO + kD * t, tmem + 128 * t + kk * 8, desc_mnmajor(vd, kk),
+                    const uint32_t pcol = kSepP ? Cfg::kTmemP + 64 * t : 128 * t;
+                    mma_ts_e(tmem + Cfg::kTmemO + kD * t, tmem + pcol + kk * 8, desc_mnmajor(vd, kk),
                              idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
                 }
             }
@@ -209,8 +250,35 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int j = 0; j < nkmax; ++j) {
             stress_delay(3, j);
-            wait_kv(2 * j + 1);
             bool k_next = false;
+            if constexpr (kSepP) {
+                // S_t(j+1) as soon as the softmax read S_t(j); then P V of tile j
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    if (j + 1 < nk[t]) {
+                        if (!k_next) {
+                            wait_kv(2 * j + 2);
+                            k_next = true;
+                        }
+                        mbar_wait_mma(s_free + t, j & 1);
+                        tc_fence_after();
+                        VTRACE(8 * j + 4 * t + 1);
+                        issue_s(t, j + 1);
+                    }
+                }
+                wait_kv(2 * j + 1);
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    if (j < nk[t]) {
+                        issue_pv(t, j);
+                        VTRACE(8 * j + 4 * t + 0);
+                    }
+                }
+                mma_commit_e(kv_empty + (2 * j + 1) % S);
+                if (k_next) mma_commit_e(kv_empty + (2 * j + 2) % S);
+                continue;
+            }
+            wait_kv(2 * j + 1);
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
                 if (j < nk[t]) {
@@ -229,42 +297,69 @@ __global__ void __launch_bounds__(384, 1)
             mma_commit_e(kv_empty + (2 * j + 1) % S);
             if (k_next) mma_commit_e(kv_empty + (2 * j + 2) % S);
         }
-    } else if (warp >= 4) {
+    } else if (warp >= Cfg::kMathWarp0) {
         // ----------------------------------------------------------- softmax
-        regs_inc<208>();
-        const int t = (warp - 4) >> 2;           // Q tile of this warpgroup
+        // Warpgroup g: Q tile t = g / kH, key-column half c = g % kH (kC columns of S,
+        // kD / kH columns of O, P quarters [kQ c, kQ c + kQ)).  Thread = query row = TMEM
+        // lane.  With two halves the row max and the final row sum are exchanged
+        // through shared memory (one 256-thread named barrier per step).
+        regs_inc<Cfg::kRegsHi>();
+        constexpr int kH = Cfg::kHalves;
+        constexpr int kC = 128 / kH;             // S columns per warpgroup
+        constexpr int kQ = 4 / kH;               // P quarters per warpgroup
+        constexpr int kOC = kD / kH;             // O columns per warpgroup
+        const int g = (warp - Cfg::kMathWarp0) >> 2;
+        const int t = g / kH;                    // Q tile of this warpgroup
+        const int c = g % kH;                    // column half
         const int r = ((warp & 3) << 5) + lane;  // row within tile == TMEM lane
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-        const uint32_t tS = tmem + lane_base + 128 * t;
-        const uint32_t tO = tmem + lane_base + Cfg::kTmemO + kD * t;
+        const uint32_t tS = tmem + lane_base + 128 * t + kC * c;
+        const uint32_t tO = tmem + lane_base + Cfg::kTmemO + kD * t + kOC * c;
+        // P_t (16-bit pairs, 64 columns per tile; quarter q at +16 q)
+        const uint32_t tP = (kSepP ? tmem + lane_base + Cfg::kTmemP + 64 * t : tmem + lane_base + 128 * t) + 16 * kQ * c;
+        const uint32_t xbar = 3 + t;             // named barrier of the tile's warpgroups
+        auto xslot = [&](int slot, int half) { return sX + ((slot * 2 + t) * kH + half) * 128; };
         const int row = q0 + 128 * t + r;
         const float sc = p.scale_log2;
         DropRow drow{};
         if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H), row);
         float m_run = -INFINITY;  // running max, log2 units (already scaled)
-        float l_run = 0.0f;
+        float l_run = 0.0f;       // this half's row sum
         bool bad = false;         // a NaN or +inf score in this row (FMNMX.NAN keeps NaN in mx)
         const int ntile = t ? nk[1] : nk[0];
         for (int j = 0; j < ntile; ++j) {
             mbar_wait<VATTN_SLEEP_MATH>(s_full + t, j & 1);
             // O += P V of the previous tile has landed (issued before S(j), so this wait
             // returns at once): observing every o_done phase in order keeps the parity
-            // waits unambiguous by construction (compute-sanitizer synccheck clean)
-            if (j > 0) mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (j - 1) & 1);
+            // waits unambiguous by construction (compute-sanitizer synccheck clean).
+            // kSepP: S(j) is issued before P V(j-1), so that wait moves to just before O
+            // or the P region is first touched in this step (o_wait below).
+            if (!kSepP && j > 0) mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (j - 1) & 1);
             tc_fence_after();
+            bool o_waited = !kSepP || j == 0;
+            auto o_wait = [&] {
+                if (!o_waited) {
+                    mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (j - 1) & 1);
+                    tc_fence_after();
+                    o_waited = true;
+                }
+            };
             stress_delay(1, j);
-            if ((warp & 3) == 0 && lane == 0) VTRACE(1024 + 8 * j + 4 * t + 0);
+            if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE(1024 + 8 * j + 4 * t + 0);
             uint4 kw4 = make_uint4(0u, 0u, 0u, 0u);  // this row's keep bits of key tile j
             if (kDrop && p.drop_mask && row < p.mask_words * 32)
                 kw4 = __ldg(reinterpret_cast<const uint4*>(p.drop_mask + (static_cast<size_t>(bh) * p.mask_words * 32 + row) *
                                                                              p.mask_words + j * 4));
-            float s[128];
-            tmem_ld32f(tS + 0, s);
-            tmem_ld32f(tS + 32, s + 32);
-            tmem_ld32f(tS + 64, s + 64);
-            tmem_ld32f(tS + 96, s + 96);
+            float s[kC];
+#pragma unroll
+            for (int x = 0; x < kC / 32; ++x) tmem_ld32f(tS + 32 * x, s + 32 * x);
             tmem_wait_ld();
-            if ((warp & 3) == 0 && lane == 0) VTRACE(2048 + 8 * j + 4 * t + 0);
+            if constexpr (kSepP) {  // S_t(j) is in registers: the MMA may overwrite it with S_t(j+1)
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(s_free + t);
+            }
+            if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE(2048 + 8 * j + 4 * t + 0);
             // (tile-uniform) masking: causal diagonal tile (keys > row) or keys beyond N
             const bool tile_masked = p.causal ? (j == ntile - 1) : (j == p.n_kv - 1 && (N & 127) != 0);
             int lim = 127;
@@ -272,46 +367,53 @@ __global__ void __launch_bounds__(384, 1)
             if (!p.causal && j == p.n_kv - 1) lim = min(lim, N - j * 128 - 1);
             if (tile_masked) {
 #pragma unroll
-                for (int c = 0; c < 128; ++c)
-                    if (c > lim) s[c] = -INFINITY;
+                for (int x = 0; x < kC; ++x)
+                    if (kC * c + x > lim) s[x] = -INFINITY;
             }
-            // row max: tree of 3-input maxima
-            const float mx = row_max<128>(s);
+            // row max: tree of 3-input maxima, then (two halves) the other half's through smem
+            float mx = row_max<kC>(s);
+            if constexpr (kH == 2) {
+                xslot(j & 1, c)[r] = mx;
+                named_bar_sync(xbar, 256);  // also: every S column of the tile is in registers
+                mx = fmax_nr(mx, xslot(j & 1, c ^ 1)[r]);
+            }
             bad |= !(mx < INFINITY);
             const float m_tile = mx * sc;
-            if ((warp & 3) == 0 && lane == 0) VTRACE(2048 + 8 * j + 4 * t + 1);
+            if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE(2048 + 8 * j + 4 * t + 1);
             if (j == 0) {
                 m_run = m_tile;
             } else if (__any_sync(0xffffffffu, m_tile > m_run + 8.0f)) {
-                // Lazy rescale (warp-uniform: tcgen05.ld/st are .sync.aligned).  The
-                // previous P V must have landed before O is touched.  Rows whose max
-                // did not grow enough keep their stale max (factor 1).
+                // Lazy rescale (warp-uniform: tcgen05.ld/st are .sync.aligned; both halves of
+                // a row see the same maxima, so they take the same branch).  The previous
+                // P V must have landed before O is touched.  Rows whose max did not grow
+                // enough keep their stale max (factor 1).
                 float f = 1.0f;
                 if (m_tile > m_run) {
                     f = ex2(m_run - m_tile);
                     m_run = m_tile;
                 }
                 l_run *= f;
+                o_wait();
 #pragma unroll
-                for (int c = 0; c < kD / 32; ++c) {
+                for (int x = 0; x < kOC / 32; ++x) {
                     uint32_t u[32];
-                    tmem_ld32(tO + 32 * c, u);
+                    tmem_ld32(tO + 32 * x, u);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int x = 0; x < 32; ++x) u[x] = __float_as_uint(__uint_as_float(u[x]) * f);
-                    tmem_st32(tO + 32 * c, u);
+                    for (int y = 0; y < 32; ++y) u[y] = __float_as_uint(__uint_as_float(u[y]) * f);
+                    tmem_st32(tO + 32 * x, u);
                 }
             }
             const float m_use = m_run == -INFINITY ? 0.0f : m_run;
-            if ((warp & 3) == 0 && lane == 0) VTRACE(2048 + 8 * j + 4 * t + 2);
+            if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE(2048 + 8 * j + 4 * t + 2);
             const float2 sc2 = make_float2(sc, sc);
             const float2 nm2 = make_float2(-m_use, -m_use);
             float2 ls2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};  // row-sum partials
-            // P in four 32-key quarters (16 packed columns each); the MMA warp
-            // starts P V on a quarter as soon as it lands.  The tensor-memory store
-            // of quarter q completes (wait::st) while quarter q+1 is computed, so
-            // the store latency never sits on the softmax's critical path.
-            auto quarter = [&](int qq, uint32_t (&pk)[16], auto poly_pair) {
+            // P in 32-key quarters (16 packed columns each); the MMA warp starts P V on a
+            // quarter as soon as it lands.  The tensor-memory store of one quarter
+            // completes (wait::st) while the next is computed.
+            auto quarter = [&](int qi, uint32_t (&pk)[16], auto poly_pair) {
+                const int qq = kQ * c + qi;  // quarter of the tile row
                 uint32_t kw = qq == 0 ? kw4.x : qq == 1 ? kw4.y : qq == 2 ? kw4.z : kw4.w;
                 if (kDrop && !p.drop_mask) {  // no pre-hashed bits: hash this quarter's 32 keys here
                     kw = 0;
@@ -321,8 +423,8 @@ __global__ void __launch_bounds__(384, 1)
                 }
 #pragma unroll
                 for (int x = 0; x < 16; ++x) {
-                    const int c = 32 * qq + 2 * x;
-                    const float2 v = ffma2(make_float2(s[c], s[c + 1]), sc2, nm2);
+                    const int e = 32 * qi + 2 * x;
+                    const float2 v = ffma2(make_float2(s[e], s[e + 1]), sc2, nm2);
                     float2 pp;
                     if (poly_pair(qq * 16 + x)) {
                         pp = ex2_poly2(v);
@@ -342,30 +444,26 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 (void)kw;
             };
-            auto publish = [&](int qq) {  // quarter qq's tcgen05.st has been waited on
+            auto publish = [&](int qi) {  // quarter qi's tcgen05.st has been waited on
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(p_full + 4 * t + qq);
-                if ((warp & 3) == 0 && lane == 0) VTRACE((qq < 3 ? 1024 + 1 + qq : 2048 + 3) + 8 * j + 4 * t);
+                if (lane == 0) mbar_arrive(p_full + 4 * t + kQ * c + qi);
+                if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE((qi < 3 ? 1024 + 1 + qi : 2048 + 3) + 8 * j + 4 * t);
             };
             auto emit_row = [&](auto poly_pair) {
                 uint32_t pa[16], pb[16];
                 quarter(0, pa, poly_pair);
-                tmem_st16(tS + 0, pa);
-                quarter(1, pb, poly_pair);
+                o_wait();  // (kSepP) P V(j-1) has read the P region
+                tmem_st16(tP + 0, pa);
+#pragma unroll
+                for (int qi = 1; qi < kQ; ++qi) {
+                    quarter(qi, (qi & 1) ? pb : pa, poly_pair);
+                    tmem_wait_st();
+                    publish(qi - 1);
+                    tmem_st16(tP + 16 * qi, (qi & 1) ? pb : pa);
+                }
                 tmem_wait_st();
-                publish(0);
-                tmem_st16(tS + 16, pb);
-                quarter(2, pa, poly_pair);
-                tmem_wait_st();
-                publish(1);
-                tmem_st16(tS + 32, pa);
-                quarter(3, pb, poly_pair);
-                tmem_wait_st();
-                publish(2);
-                tmem_st16(tS + 48, pb);
-                tmem_wait_st();
-                publish(3);
+                publish(kQ - 1);
             };
             constexpr int kPer = PolyPeriod<kD>::fwd;
             auto poly_fast = [](int pair) {
@@ -384,32 +482,38 @@ __global__ void __launch_bounds__(384, 1)
             // ------------------------------------------------------ epilogue
             mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (ntile - 1) & 1);
             tc_fence_after();
-            const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+            float l_tot = l_run;
+            if constexpr (kH == 2) {  // the row sum over both halves
+                xslot(2, c)[r] = l_run;
+                named_bar_sync(xbar, 256);
+                l_tot += xslot(2, c ^ 1)[r];
+            }
+            const float inv_l = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
             if (row < N) {
                 const float m_use = m_run == -INFINITY ? 0.0f : m_run;
-                p.lse[static_cast<size_t>(bh) * N + row] = (m_use + lg2(l_run)) * 0.69314718055994530942f;
-                if (p.status && (bad || !(l_run > 0.0f))) atomicOr(p.status, 1u);
+                if (c == 0) p.lse[static_cast<size_t>(bh) * N + row] = (m_use + lg2(l_tot)) * 0.69314718055994530942f;
+                if (p.status && (bad || !(l_tot > 0.0f))) atomicOr(p.status, 1u);
             }
             uint8_t* sO = sQ + t * Cfg::kTileBytes;  // Q_t is dead once the last S_t landed
 #pragma unroll
-            for (int c = 0; c < kD / 32; ++c) {
+            for (int x = 0; x < kOC / 32; ++x) {
                 uint32_t u[32];
-                tmem_ld32(tO + 32 * c, u);
+                tmem_ld32(tO + 32 * x, u);
                 tmem_wait_ld();
 #pragma unroll
-                for (int x = 0; x < 4; ++x) {
+                for (int y = 0; y < 4; ++y) {
                     uint4 v;
-                    v.x = pack2<kBF16>(__uint_as_float(u[8 * x + 0]) * inv_l, __uint_as_float(u[8 * x + 1]) * inv_l);
-                    v.y = pack2<kBF16>(__uint_as_float(u[8 * x + 2]) * inv_l, __uint_as_float(u[8 * x + 3]) * inv_l);
-                    v.z = pack2<kBF16>(__uint_as_float(u[8 * x + 4]) * inv_l, __uint_as_float(u[8 * x + 5]) * inv_l);
-                    v.w = pack2<kBF16>(__uint_as_float(u[8 * x + 6]) * inv_l, __uint_as_float(u[8 * x + 7]) * inv_l);
-                    const int col = 32 * c + 8 * x;  // first of 8 columns
+                    v.x = pack2<kBF16>(__uint_as_float(u[8 * y + 0]) * inv_l, __uint_as_float(u[8 * y + 1]) * inv_l);
+                    v.y = pack2<kBF16>(__uint_as_float(u[8 * y + 2]) * inv_l, __uint_as_float(u[8 * y + 3]) * inv_l);
+                    v.z = pack2<kBF16>(__uint_as_float(u[8 * y + 4]) * inv_l, __uint_as_float(u[8 * y + 5]) * inv_l);
+                    v.w = pack2<kBF16>(__uint_as_float(u[8 * y + 6]) * inv_l, __uint_as_float(u[8 * y + 7]) * inv_l);
+                    const int col = kOC * c + 32 * x + 8 * y;  // first of 8 columns
                     st_swz128(sO + (col >> 6) * 16384, r, (col & 63) >> 3, v);
                 }
             }
             fence_proxy_async_smem();
-            named_bar_sync(1 + t, 128);
-            if (warp == 4 + 4 * t && lane == 0) {
+            named_bar_sync(xbar, 128 * kH);
+            if (warp == Cfg::kMathWarp0 + 4 * kH * t && lane == 0) {
                 for (int b = 0; b < Cfg::kBoxes; ++b)
                     tma_store_3d(&tm_o, sO + b * 16384, b * 64, q0 + 128 * t, bh);
                 bulk_commit();
@@ -420,7 +524,7 @@ __global__ void __launch_bounds__(384, 1)
     griddep_launch_dependents();
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == Cfg::kAllocWarp) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
     }

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2502_12784_b200 as vb  # noqa: E402  (config struct only)
 
-lib = C.CDLL(os.path.join(ROOT, "tools", "libvattn_b200_trace.so"))
+lib = C.CDLL(os.environ.get("VATTN_TRACE_LIB") or os.path.join(ROOT, "tools", "libvattn_b200_trace.so"))
 B, H, N, d, causal = (int(x) for x in sys.argv[1:6])
 block = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 dt = torch.bfloat16
