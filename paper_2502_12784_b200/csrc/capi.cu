@@ -316,12 +316,9 @@ int bh_group(int BH, long long per_unit_bytes, bool fwd) {
 // otherwise start in the final wave and leave a ~60 us per-SM tail at C3).  The rest
 // stays unit-major: all key tiles of one unit share its Q/dO stream in L2 (a fully
 // grouped order measured 3 % slower per CTA).  VATTN_DKDV_TAIL_WAVES overrides (0 = off).
-int dkdv_tail_units(int BH, int n_q, int ctas_per_item = 1) {
-    static const double waves = [] {
-        const char* e = getenv("VATTN_DKDV_TAIL_WAVES");
-        return e ? atof(e) : 3.5;
-    }();
-    static std::atomic<int> sm_count[64] = {};  // per device; racing writers store the same value
+// SM count of the current device (cached per device; racing writers store the same value).
+int sm_count_cached() {
+    static std::atomic<int> sm_count[64] = {};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
     int sms = sm_count[dev].load(std::memory_order_relaxed);
@@ -329,6 +326,15 @@ int dkdv_tail_units(int BH, int n_q, int ctas_per_item = 1) {
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
         sm_count[dev].store(sms, std::memory_order_relaxed);
     }
+    return sms;
+}
+
+int dkdv_tail_units(int BH, int n_q, int ctas_per_item = 1) {
+    static const double waves = [] {
+        const char* e = getenv("VATTN_DKDV_TAIL_WAVES");
+        return e ? atof(e) : 3.5;
+    }();
+    const int sms = sm_count_cached();
     const int T = static_cast<int>((waves * (sms / ctas_per_item) + n_q - 1) / n_q);
     return T < 0 ? 0 : (T > BH ? BH : T);
 }
@@ -445,7 +451,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
 }
 
 struct BwdLayout {
-    size_t lse2, dsum, ds, mask, total;
+    size_t lse2, dsum, ds, sync, mask, total;
     bool drop_mask;          // dropout keep bits hashed once into the workspace
     int n_q, Npad;
     bool materialize_ds;     // dQ as a GEMM over materialised dS (else recompute S, dP)
@@ -514,7 +520,8 @@ BwdLayout bwd_layout(const vattn_config* c) {
     L.materialize_ds = c->dropout_p > 0.0f && !L.drop_mask
                            ? false
                            : (mode_env >= 0 ? mode_env == 1 : ((c->head_dim == 128 || c->seq_len <= 1024) && ds_bytes <= ds_cap_bytes()));
-    L.mask = L.ds + (L.materialize_ds ? align256(ds_bytes) : 0);
+    L.sync = L.ds + (L.materialize_ds ? align256(ds_bytes) : 0);  // dQ hand-off words (BwdParams::dq_sync)
+    L.mask = L.sync + (L.materialize_ds ? align256((2 + BH) * sizeof(int)) : 0);
     L.total = L.mask + (L.drop_mask ? align256(mask_bytes) : 0);
     return L;
 }
@@ -544,7 +551,8 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         if (blocks > 148 * 8) blocks = 148 * 8;
         ProfScope prof(stream, 3);
         launch_pdl(mha_bwd_preprocess_kernel<kD, kBF16>, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream,
-                   o, dout, lse, lse2, dsum, N, L.Npad, BH);
+                   o, dout, lse, lse2, dsum, N, L.Npad, BH, L.materialize_ds ? reinterpret_cast<int*>(w + L.sync) : nullptr,
+                   L.materialize_ds ? 2 + BH : 0);
     }
     BwdParams p;
     p.lse2 = lse2;
@@ -568,6 +576,26 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     }();
     const bool pair = kD == 128 && pair_env;
     const int n_pairs = (L.n_q + 1) / 2;
+    // VATTN_DQ_WORKERS=W > 0: dQ overlapped with dK/dV (dS materialised, one CTA per key
+    // tile): the first W CTAs of the dK/dV grid are persistent dQ workers (mha_bwd_sm100.cuh
+    // dq_worker) taking units as their dS^T tiles complete; a full-width tail launch
+    // finishes the rest.  Bitwise identical; measured neutral (C3 step 3.87 ms for W = 0,
+    // 8, 16, 24: a dQ worker moves ~45 GB/s whether 24 or 148 SMs run it, so the dQ work
+    // hidden equals the dK/dV work displaced -- profiles/r2_experiments.md).  Default 0:
+    // the separate dQ GEMM launch.
+    static const int workers_env = [] {
+        const char* e = getenv("VATTN_DQ_WORKERS");
+        return e ? atoi(e) : 0;
+    }();
+    const int sms = sm_count_cached();
+    int W = workers_env;
+    if (!L.materialize_ds || pair) W = 0;
+    if (W > sms / 2) W = sms / 2;
+    p.dq_sync = W > 0 ? reinterpret_cast<int*>(w + L.sync) : nullptr;
+    p.dq_workers = W;
+    p.dkdv_ctas = L.n_q * BH;
+    p.n_units = BH;
+    p.ds_signals = DkdvCfg<kD>::kWG * L.n_q;
     p.tail_units = c->causal ? (pair ? dkdv_tail_units(BH, n_pairs, 2) : dkdv_tail_units(BH, L.n_q)) : 0;
     p.drop_mask = nullptr;
     p.drop_mask_k = nullptr;
@@ -599,21 +627,31 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
         launch_pdl_pair(kern, dim3(2 * n_pairs * BH), dim3(DkdvCfg<kD>::kThreads), smem, stream, mq, mk, mv, mdo,
-                        L.materialize_ds ? mds : mq, mq64, mdo64, dk, dv, p);
+                        L.materialize_ds ? mds : mq, mq64, mdo64, mdq, dk, dv, p);
         dkdv_launched = true;
       }
     }
     if (!dkdv_launched) {
         auto kern = mha_bwd_dkdv_kernel<kD, kBF16, kDrop>;
-        constexpr int smem = DkdvCfg<kD>::kSmemBytes;
+        // (the dQ workers' layout may be the larger one)
+        constexpr int smem = DkdvCfg<kD>::kSmemBytes > DqGemmCfg<kD>::kSmemBytes ? DkdvCfg<kD>::kSmemBytes
+                                                                                 : DqGemmCfg<kD>::kSmemBytes;
         const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
-        launch_pdl(kern, dim3(L.n_q * BH), dim3(DkdvCfg<kD>::kThreads), smem, stream, mq, mk, mv, mdo,
-                   L.materialize_ds ? mds : mq, mq, mdo, dk, dv, p);
+        launch_pdl(kern, dim3(L.n_q * BH + W), dim3(DkdvCfg<kD>::kThreads), smem, stream, mq, mk, mv, mdo,
+                   L.materialize_ds ? mds : mq, mq, mdo, mdq, dk, dv, p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)
-    if (L.materialize_ds) {
+    if (W > 0) {  // what the overlapped workers left: full width
+        auto kern = mha_bwd_dq_tail_kernel<kD, kBF16>;
+        constexpr int smem = DqGemmCfg<kD>::kSmemBytes;
+        const cudaError_t ae = set_smem_once<mha_bwd_dq_tail_kernel<kD, kBF16>>(smem);
+        if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
+        ProfScope prof(stream, 2);
+        const int items = L.n_q * BH;
+        launch_pdl(kern, dim3(items < sms ? items : sms), dim3(256), smem, stream, mds, mk, mdq, p);
+    } else if (L.materialize_ds) {
         auto kern = mha_bwd_dq_gemm_kernel<kD, kBF16>;
         constexpr int smem = DqGemmCfg<kD>::kSmemBytes;
         const cudaError_t ae = set_smem_once<mha_bwd_dq_gemm_kernel<kD, kBF16>>(smem);
@@ -793,17 +831,17 @@ int mha_dpsum(const vattn_config* cfg, const void* o, const void* dout, float* d
     if (cfg->head_dim == 128) {
         if (cfg->dtype == VATTN_BF16)
             launch_pdl(mha_bwd_preprocess_kernel<128, true>, grid, dim3(256), 0, s, o, dout, (const float*)nullptr,
-                       (float*)nullptr, d_rows, N, N, BH);
+                       (float*)nullptr, d_rows, N, N, BH, (int*)nullptr, 0);
         else
             launch_pdl(mha_bwd_preprocess_kernel<128, false>, grid, dim3(256), 0, s, o, dout, (const float*)nullptr,
-                       (float*)nullptr, d_rows, N, N, BH);
+                       (float*)nullptr, d_rows, N, N, BH, (int*)nullptr, 0);
     } else {
         if (cfg->dtype == VATTN_BF16)
             launch_pdl(mha_bwd_preprocess_kernel<64, true>, grid, dim3(256), 0, s, o, dout, (const float*)nullptr,
-                       (float*)nullptr, d_rows, N, N, BH);
+                       (float*)nullptr, d_rows, N, N, BH, (int*)nullptr, 0);
         else
             launch_pdl(mha_bwd_preprocess_kernel<64, false>, grid, dim3(256), 0, s, o, dout, (const float*)nullptr,
-                       (float*)nullptr, d_rows, N, N, BH);
+                       (float*)nullptr, d_rows, N, N, BH, (int*)nullptr, 0);
     }
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = g_launch_err;

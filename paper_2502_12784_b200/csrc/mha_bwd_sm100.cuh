@@ -32,7 +32,8 @@ namespace vattn_sm100 {
 template <int kD, bool kBF16>
 __global__ void __launch_bounds__(256) mha_bwd_preprocess_kernel(
     const void* __restrict__ o, const void* __restrict__ dout, const float* __restrict__ lse,
-    float* __restrict__ lse2, float* __restrict__ dsum, int N, int Npad, int BH) {
+    float* __restrict__ lse2, float* __restrict__ dsum, int N, int Npad, int BH, int* __restrict__ zero = nullptr,
+    int zero_n = 0) {
     using T16 = typename std::conditional<kBF16, __nv_bfloat16, __half>::type;
     constexpr int kLanesPerRow = kD / 8;
     constexpr int kRowsPerWarp = 32 / kLanesPerRow;
@@ -43,6 +44,10 @@ __global__ void __launch_bounds__(256) mha_bwd_preprocess_kernel(
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const long long rows = static_cast<long long>(BH) * Npad;
     griddep_wait();  // O / lse come from the forward kernel
+    // the dQ hand-off words of this backward (BwdParams::dq_sync): the dK/dV kernel reads
+    // them only after its griddep_wait, i.e. after this grid completed
+    if (zero && blockIdx.x == 0)
+        for (int x = threadIdx.x; x < zero_n; x += blockDim.x) zero[x] = 0;
     for (long long r0 = static_cast<long long>(gw) * kRowsPerWarp * kU; r0 < rows;
          r0 += static_cast<long long>(nwarps) * kRowsPerWarp * kU) {
         long long row[kU];
@@ -115,6 +120,15 @@ struct BwdParams {
     // [unit][key][Npad/32 words] (bit = query).
     const uint32_t* drop_mask;
     const uint32_t* drop_mask_k;
+    // dQ overlapped with dK/dV (ds_out only): the first dq_workers CTAs of the dK/dV grid
+    // run the dQ GEMM over units whose dS^T tiles are complete; the rest of the grid is
+    // the dK/dV items.  dq_sync = [0] next dQ item, [1] finished dK/dV CTAs, [2 + u]
+    // finished dS^T stores of unit u (2 per key tile).  nullptr = dQ is a separate launch.
+    int* dq_sync;
+    int dq_workers;
+    int dkdv_ctas;
+    int n_units;        // (b, h) units of this launch
+    int ds_signals;     // dS^T store-done signals per unit (store threads per key tile x n_q)
 };
 
 // Dropout keep bits, hashed once per step ahead of the forward: the reference's
@@ -193,6 +207,182 @@ __global__ void __launch_bounds__(256) mha_dropmask_kernel(uint32_t* __restrict_
 // Index of dS^T tile (query tile i, key tile kb) within one (b, h).
 VATTN_DEV long long ds_tile_index(const BwdParams& p, int i, int kb) {
     return p.causal ? static_cast<long long>(i) * (i + 1) / 2 + kb : static_cast<long long>(i) * p.n_q + kb;
+}
+
+// ============================================================ dQ GEMM ==
+//
+// dQ_i = sum_j dS_ij K_j from the dS^T tiles the dK/dV kernel materialised (d = 128, or
+// d = 64 with N <= 1024): A = dS^T tile (MN-major), B = K_j (MN-major), accumulated in
+// tensor memory in ascending j (the reference's DqAccumulator order) and rounded once.
+template <int kD>
+struct DqGemmCfg {
+    static constexpr int kKBytes = kD * 128 * 2;
+    static constexpr int kDsBytes = 128 * 128 * 2;
+    static constexpr int kStageBytes = kKBytes + kDsBytes;
+    static constexpr int kStages = kD == 128 ? 3 : 4;
+    static constexpr int kSmemOut = kStages * kStageBytes;       // persistent worker: dQ staging
+    static constexpr int kSmemBar = kSmemOut + kD * 128 * 2;
+    static constexpr int kNumBars = 2 * kStages + 1;
+    static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
+};
+
+VATTN_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Persistent dQ worker (256 threads: warp 0 TMA, warp 1 MMA, warp 2 TMEM, warps 4-7
+// epilogue).  Items = (unit, query tile), unit-major, longest causal tile first, taken
+// from the atomic counter dq_sync[0].  `early` workers are CTAs of the dK/dV grid: they
+// wait until every dS^T store of the item's unit is done (dq_sync[2 + u]) and stop
+// taking items once all dK/dV CTAs have finished (dq_sync[1]), leaving the rest to the
+// full-width mha_bwd_dq_tail_kernel launched after the dK/dV grid.  Same arithmetic and
+// accumulation order as one dQ tile per CTA: results are bitwise identical.
+template <int kD, bool kBF16>
+VATTN_DEV void dq_worker(const CUtensorMap* tm_ds, const CUtensorMap* tm_k, const CUtensorMap* tm_dq, const BwdParams& p,
+                         uint8_t* smem, bool early) {
+    using Cfg = DqGemmCfg<kD>;
+    constexpr int S = Cfg::kStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kSmemBar);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* dq_done = bars + 2 * S;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
+    volatile int* s_item = reinterpret_cast<volatile int*>(tmem_slot + 1);
+    const int warp = warp_id();
+    const int lane = lane_id();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(dq_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<kD>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    griddep_wait();  // dq_sync zeroed / dS^T written by the previous kernels in the stream
+    const int nq = p.n_q;
+    const int total = p.n_units * nq;
+    uint32_t pos = 0, it = 0;  // ring position (tiles) and items done by this CTA
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(tm_ds);
+        tma_prefetch_desc(tm_k);
+        tma_prefetch_desc(tm_dq);
+    }
+    for (;;) {
+        if (threadIdx.x == 0) {
+            int item = -1;
+            if (!early || ld_acquire_gpu(p.dq_sync + 1) < p.dkdv_ctas) {
+                item = atomicAdd(p.dq_sync, 1);
+                if (item >= total) {
+                    item = -1;
+                } else if (early) {
+                    const int* cnt = p.dq_sync + 2 + item / nq;
+                    const uint64_t t0 = globaltimer_ns();
+                    while (ld_acquire_gpu(cnt) < p.ds_signals) {
+                        __nanosleep(500);
+                        if (globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) __trap();
+                    }
+                    fence_proxy_async_global();  // the TMA loads below see the dS^T stores
+                }
+            }
+            *s_item = item;
+        }
+        __syncthreads();
+        const int item = *s_item;
+        if (item < 0) break;
+        const int bh = item / nq, tile = item - bh * nq;
+        const int i = p.causal ? (nq - 1 - tile) : tile;
+        const int nk = p.causal ? i + 1 : nq;
+        if (warp == 0) {
+            if (lane == 0) {
+                const long long tile0 = static_cast<long long>(bh) * p.ds_tiles_per_bh + ds_tile_index(p, i, 0);
+                for (int j = 0; j < nk; ++j) {
+                    const uint32_t q = pos + j;
+                    const int st = q % S;
+                    mbar_wait<VATTN_SLEEP_PRODUCER>(empty + st, ((q / S) & 1) ^ 1);
+                    mbar_arrive_expect_tx(full + st, Cfg::kStageBytes);
+                    uint8_t* ds = smem + st * Cfg::kStageBytes;
+                    uint8_t* kt = ds + Cfg::kDsBytes;
+                    const int tl = static_cast<int>(tile0 + j);
+                    tma_load_3d(ds, tm_ds, full + st, 0, 0, tl);
+                    tma_load_3d(ds + 16384, tm_ds, full + st, 64, 0, tl);
+                    for (int b = 0; b < kD / 64; ++b) tma_load_3d(kt + b * 16384, tm_k, full + st, b * 64, j * 128, bh);
+                }
+            }
+        } else if (warp == 1) {
+            constexpr uint32_t idesc = umma_idesc_f16(128, kD, kBF16, 1, 1);  // A = dS (MN-major), B = K (MN-major)
+            const uint64_t dA0 = umma_desc_sw128(smem_u32(smem), 16384, 1024);
+            const uint64_t dB0 = umma_desc_sw128(smem_u32(smem + Cfg::kDsBytes), 16384, 1024);
+            constexpr uint64_t kStage16 = Cfg::kStageBytes >> 4;
+            for (int j = 0; j < nk; ++j) {
+                const uint32_t q = pos + j;
+                const int st = q % S;
+                mbar_wait_mma(full + st, (q / S) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_ss_e(tmem, desc_mnmajor(dA0 + st * kStage16, kk), desc_mnmajor(dB0 + st * kStage16, kk), idesc,
+                             (j > 0 || kk > 0) ? 1u : 0u);
+                mma_commit_e(empty + st);
+            }
+            mma_commit_e(dq_done);
+        } else if (warp >= 4 && warp < 8) {
+            // dQ * scale -> 16-bit -> swizzled staging -> TMA store
+            const int r = ((warp & 3) << 5) + lane;
+            const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
+            uint8_t* sOut = smem + Cfg::kSmemOut;
+            if (warp == 4 && lane == 0) bulk_wait_read0();  // the previous item's store left the staging
+            mbar_wait<VATTN_SLEEP_MATH>(dq_done, it & 1);
+            tc_fence_after();
+            named_bar_sync(1, 128);
+#pragma unroll
+            for (int c = 0; c < kD / 32; ++c) {
+                float a[32];
+                tmem_ld32f(tmem + lb + 32 * c, a);
+                tmem_wait_ld();
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    uint4 v;
+                    v.x = pack2<kBF16>(a[8 * x + 0] * p.scale, a[8 * x + 1] * p.scale);
+                    v.y = pack2<kBF16>(a[8 * x + 2] * p.scale, a[8 * x + 3] * p.scale);
+                    v.z = pack2<kBF16>(a[8 * x + 4] * p.scale, a[8 * x + 5] * p.scale);
+                    v.w = pack2<kBF16>(a[8 * x + 6] * p.scale, a[8 * x + 7] * p.scale);
+                    const int cc = 32 * c + 8 * x;
+                    st_swz128(sOut + (cc >> 6) * 16384, r, (cc & 63) >> 3, v);
+                }
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            if (warp == 4 && lane == 0) {
+                for (int b = 0; b < kD / 64; ++b) tma_store_3d(tm_dq, sOut + b * 16384, b * 64, i * 128, bh);
+                bulk_commit();
+            }
+        }
+        pos += static_cast<uint32_t>(nk);
+        ++it;
+        tc_fence_before();
+        __syncthreads();  // TMEM read out before the next item's first MMA; s_item reuse
+        tc_fence_after();
+    }
+    if (warp == 4 && lane == 0) bulk_wait_read0();  // no store reads smem past exit
+    griddep_launch_dependents();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<kD>(tmem);
+    }
+}
+
+// Full-width tail of the overlapped dQ: every unit is complete when it starts.
+template <int kD, bool kBF16>
+__global__ void __launch_bounds__(256, 1)
+    mha_bwd_dq_tail_kernel(const __grid_constant__ CUtensorMap tm_ds, const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    dq_worker<kD, kBF16>(&tm_ds, &tm_k, &tm_dq, p, smem, false);
 }
 
 // ================================================================ dK / dV ==
@@ -277,10 +467,18 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                         const __grid_constant__ CUtensorMap tm_ds,
                         const __grid_constant__ CUtensorMap tm_q64,   // 64-row boxes (kPair)
                         const __grid_constant__ CUtensorMap tm_do64,  // 64-row boxes (kPair)
+                        const __grid_constant__ CUtensorMap tm_dq,    // dQ (dq_workers > 0)
                         void* __restrict__ dk_out, void* __restrict__ dv_out, const BwdParams p) {
     VCTA(1, 0);
     using Cfg = DkdvCfg<kD>;
     static_assert(!kPair || (kD == 128 && !Cfg::kDoubleS), "CTA pair: d = 128 only");
+    if constexpr (!kPair) {  // the grid's first dq_workers CTAs overlap the dQ GEMM (see dq_worker)
+        if (static_cast<int>(blockIdx.x) < p.dq_workers) {
+            extern __shared__ __align__(1024) uint8_t smem_dq[];
+            dq_worker<kD, kBF16>(&tm_ds, &tm_k, &tm_dq, p, smem_dq, true);
+            return;
+        }
+    }
     constexpr int kVtraceKid = 1;
     (void)kVtraceKid;
     using T16 = typename std::conditional<kBF16, __nv_bfloat16, __half>::type;
@@ -329,7 +527,8 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                          p.tail_units, bh, pr);
         kb = 2 * pr + static_cast<int>(rank);
     } else {
-        grid_item_tail(p.n_q, p.tail_units, bh, kb);
+        grid_item_tail_n(static_cast<int>(blockIdx.x) - p.dq_workers, static_cast<int>(gridDim.x) - p.dq_workers, p.n_q,
+                         p.tail_units, bh, kb);
     }
     const int N = p.N;
     // causal: both CTAs of a pair start at the lower key tile's diagonal (the upper
@@ -752,7 +951,16 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
 
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 3);
         }
-        if (p.ds_out && (warp & 3) == 0 && lane == 0) bulk_wait_read0();  // no store reads smem past exit
+        if (p.ds_out && (warp & 3) == 0 && lane == 0) {
+            if (p.dq_sync) {  // this CTA's dS^T stores are in memory: count them for the dQ workers
+                bulk_wait0();
+                fence_proxy_async_global();
+                __threadfence();
+                atomicAdd(p.dq_sync + 2 + bh, 1);
+            } else {
+                bulk_wait_read0();  // no store reads smem past exit
+            }
+        }
         // ---------------------------------------------------------- epilogue
         mbar_wait(dkv_full, 0);
         tc_fence_after();
@@ -798,6 +1006,15 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
     }
     griddep_launch_dependents();
     tc_fence_before();
+    if constexpr (!kPair) {
+        if (p.dq_sync) {  // after this CTA's dS^T counts (the barrier below orders them)
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(p.dq_sync + 1, 1);
+            }
+        }
+    }
     if constexpr (kPair) {
         cluster_sync_all();  // the leader's MMAs read the peer's smem / TMEM until dkv_full
         if (warp == 2) {
@@ -1192,17 +1409,6 @@ __global__ void __launch_bounds__(384, 1)
 // tensor memory in ascending j (the same fixed order and single rounding as the
 // reference's DqAccumulator, attention_backward.cpp:205,215) -- deterministic, and
 // none of the S / dP recompute of mha_bwd_dq_kernel.  HBM-bound on the dS stream.
-template <int kD>
-struct DqGemmCfg {
-    static constexpr int kKBytes = kD * 128 * 2;
-    static constexpr int kDsBytes = 128 * 128 * 2;
-    static constexpr int kStageBytes = kKBytes + kDsBytes;
-    static constexpr int kStages = kD == 128 ? 3 : 4;
-    static constexpr int kSmemBar = kStages * kStageBytes;
-    static constexpr int kNumBars = 2 * kStages + 1;
-    static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
-};
-
 template <int kD, bool kBF16>
 __global__ void __launch_bounds__(256, 1)
     mha_bwd_dq_gemm_kernel(const __grid_constant__ CUtensorMap tm_ds, const __grid_constant__ CUtensorMap tm_k,

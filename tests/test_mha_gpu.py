@@ -367,6 +367,42 @@ def test_dkdv_cta_pair_vs_single(tmp_path):
             assert torch.equal(a, b), f"{key} {name}: pair differs from one CTA"
 
 
+_WORKERS_CHILD = r'''
+import os, sys
+sys.path.insert(0, os.environ["ROOT"])
+import torch
+import paper_2502_12784_b200 as vb
+from tests.gpu_util import workload
+out = {}
+for (B, H, N, d, causal, dtype, p) in [(2, 4, 1000, 128, True, torch.bfloat16, 0.0), (1, 3, 640, 128, False, torch.float16, 0.0),
+                                       (2, 4, 1024, 64, True, torch.float16, 0.0), (1, 2, 700, 128, True, torch.bfloat16, 0.1)]:
+    q, k, v, do = workload(41 + N, (B, H, N, d), dtype)
+    o, lse = vb.mha_forward(q, k, v, causal, dropout_p=p, seed=3)
+    out[(B, H, N, d, causal, p)] = [t.cpu() for t in vb.mha_backward(q, k, v, o, do, lse, causal, dropout_p=p, seed=3)]
+torch.save(out, os.environ["OUT"])
+print("OK")
+'''
+
+
+def test_dq_workers_overlap_bitwise(tmp_path):
+    """VATTN_DQ_WORKERS > 0 (dQ GEMM workers inside the dK/dV grid, per-unit readiness
+    counters, full-width tail launch) gives the same dQ / dK / dV bits as the separate
+    dQ GEMM launch."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for w in ("0", "12"):
+        path = str(tmp_path / f"w{w}.pt")
+        r = subprocess.run([sys.executable, "-c", _WORKERS_CHILD], capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, VATTN_DQ_WORKERS=w, ROOT=root, OUT=path))
+        assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+        res[w] = torch.load(path)
+    for key, a in res["0"].items():
+        for name, x, y in zip(("dQ", "dK", "dV"), a, res["12"][key]):
+            assert torch.equal(x, y), f"{key} {name}: overlapped dQ differs"
+
+
 # --------------------------------------- compute_dpsum and the mask digest --
 
 @pytest.mark.parametrize("d,dtype", [(64, torch.float16), (128, torch.bfloat16)])
