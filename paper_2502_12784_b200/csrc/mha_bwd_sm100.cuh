@@ -870,10 +870,14 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                     publish(0);
                 }
             };
-            if ((h & 1) == 0)  // warp-uniform
-                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DKDV64_WG0 : VATTN_POLY_DKDV_WG0>{});
+            constexpr int kPoly0 = kD == 64 ? VATTN_POLY_DKDV64_WG0 : VATTN_POLY_DKDV_WG0;
+            constexpr int kPoly1 = kD == 64 ? VATTN_POLY_DKDV64_WG1 : VATTN_POLY_DKDV_WG1;
+            if constexpr (kPoly0 == kPoly1)  // one copy of the P pass
+                p_pass(std::integral_constant<int, kPoly0>{});
+            else if ((h & 1) == 0)  // warp-uniform
+                p_pass(std::integral_constant<int, kPoly0>{});
             else
-                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DKDV64_WG1 : VATTN_POLY_DKDV_WG1>{});
+                p_pass(std::integral_constant<int, kPoly1>{});
             if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 1);
             stress_delay(2, s);
 
@@ -1289,10 +1293,14 @@ __global__ void __launch_bounds__(384, 1)
                     pr[x + 1] = a.y;
                 }
             };
-            if (h == 0)  // warp-uniform
-                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DQ64_WG0 : VATTN_POLY_DQ_WG0>{});
+            constexpr int kPoly0 = kD == 64 ? VATTN_POLY_DQ64_WG0 : VATTN_POLY_DQ_WG0;
+            constexpr int kPoly1 = kD == 64 ? VATTN_POLY_DQ64_WG1 : VATTN_POLY_DQ_WG1;
+            if constexpr (kPoly0 == kPoly1)  // one copy of the P pass
+                p_pass(std::integral_constant<int, kPoly0>{});
+            else if (h == 0)  // warp-uniform
+                p_pass(std::integral_constant<int, kPoly0>{});
             else
-                p_pass(std::integral_constant<int, kD == 64 ? VATTN_POLY_DQ64_WG1 : VATTN_POLY_DQ_WG1>{});
+                p_pass(std::integral_constant<int, kPoly1>{});
             // masks only on the (warp-uniform) causal diagonal tile / the tile holding key N-1
             if ((p.causal && j == i) || kbase + 64 > N) {
 #pragma unroll

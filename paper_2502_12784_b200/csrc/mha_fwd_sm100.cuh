@@ -100,6 +100,21 @@ struct FwdCfg {
     static constexpr bool kSepP = kD == 64 && VATTN_FWD_SEPP;  // P in its own region (see above)
     static constexpr uint32_t kTmemP = 384;          // kSepP: P_t at [384 + 64t, +64)
 };
+#ifndef VATTN_FWD_SPEC_MAX
+#define VATTN_FWD_SPEC_MAX 0
+#endif
+constexpr bool kSpecMax = VATTN_FWD_SPEC_MAX;  // speculative first quarter (see the softmax loop)
+// Masked (diagonal / ragged) tiles on MUFU only (a second unrolled copy of the softmax
+// body); 0 = the same polynomial split as every tile (ex2_poly2(-inf) is exactly 0 too).
+#ifndef VATTN_FWD_MASKED_MUFU
+#define VATTN_FWD_MASKED_MUFU 0
+#endif
+constexpr bool kMaskedMufu = VATTN_FWD_MASKED_MUFU;
+// O rescale / epilogue column loops: 1 = rolled (smaller kernel), 4 = unrolled
+#ifndef VATTN_FWD_RESCALE_UNROLL
+#define VATTN_FWD_RESCALE_UNROLL 4
+#endif
+constexpr int kRescaleUnroll = VATTN_FWD_RESCALE_UNROLL;
 
 template <int kD, bool kBF16, bool kDrop>
 __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
@@ -370,50 +385,12 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
                 for (int x = 0; x < kC; ++x)
                     if (kC * c + x > lim) s[x] = -INFINITY;
             }
-            // row max: tree of 3-input maxima, then (two halves) the other half's through smem
-            float mx = row_max<kC>(s);
-            if constexpr (kH == 2) {
-                xslot(j & 1, c)[r] = mx;
-                named_bar_sync(xbar, 256);  // also: every S column of the tile is in registers
-                mx = fmax_nr(mx, xslot(j & 1, c ^ 1)[r]);
-            }
-            bad |= !(mx < INFINITY);
-            const float m_tile = mx * sc;
-            if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE(2048 + 8 * j + 4 * t + 1);
-            if (j == 0) {
-                m_run = m_tile;
-            } else if (__any_sync(0xffffffffu, m_tile > m_run + 8.0f)) {
-                // Lazy rescale (warp-uniform: tcgen05.ld/st are .sync.aligned; both halves of
-                // a row see the same maxima, so they take the same branch).  The previous
-                // P V must have landed before O is touched.  Rows whose max did not grow
-                // enough keep their stale max (factor 1).
-                float f = 1.0f;
-                if (m_tile > m_run) {
-                    f = ex2(m_run - m_tile);
-                    m_run = m_tile;
-                }
-                l_run *= f;
-                o_wait();
-#pragma unroll
-                for (int x = 0; x < kOC / 32; ++x) {
-                    uint32_t u[32];
-                    tmem_ld32(tO + 32 * x, u);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int y = 0; y < 32; ++y) u[y] = __float_as_uint(__uint_as_float(u[y]) * f);
-                    tmem_st32(tO + 32 * x, u);
-                }
-            }
-            const float m_use = m_run == -INFINITY ? 0.0f : m_run;
-            if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE(2048 + 8 * j + 4 * t + 2);
-            const float2 sc2 = make_float2(sc, sc);
-            const float2 nm2 = make_float2(-m_use, -m_use);
+            // P of one 32-key quarter (16 packed columns) with offset mu (log2 units)
             float2 ls2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};  // row-sum partials
-            // P in 32-key quarters (16 packed columns each); the MMA warp starts P V on a
-            // quarter as soon as it lands.  The tensor-memory store of one quarter
-            // completes (wait::st) while the next is computed.
-            auto quarter = [&](int qi, uint32_t (&pk)[16], auto poly_pair) {
+            auto quarter = [&](int qi, uint32_t (&pk)[16], auto poly_pair, float mu) {
                 const int qq = kQ * c + qi;  // quarter of the tile row
+                const float2 sc2 = make_float2(sc, sc);
+                const float2 nm2 = make_float2(-mu, -mu);
                 uint32_t kw = qq == 0 ? kw4.x : qq == 1 ? kw4.y : qq == 2 ? kw4.z : kw4.w;
                 if (kDrop && !p.drop_mask) {  // no pre-hashed bits: hash this quarter's 32 keys here
                     kw = 0;
@@ -444,20 +421,80 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
                 }
                 (void)kw;
             };
+            constexpr int kPer = PolyPeriod<kD>::fwd;
+            auto poly_fast = [](int pair) {
+                if constexpr (kPer > 0) return pair % kPer == kPer - 1;
+                return false;
+            };
+            auto poly_none = [](int) { return false; };  // -inf -> exact 0 on masked tiles
+            auto quarter0 = [&](uint32_t (&pk)[16], float mu) {
+                if (kMaskedMufu && tile_masked)
+                    quarter(0, pk, poly_none, mu);
+                else
+                    quarter(0, pk, poly_fast, mu);
+            };
+            uint32_t pa[16], pb[16];
+            // Speculative first quarter (j > 0): exponentiated with the running max while the
+            // row max is still being reduced (the two are independent instruction streams);
+            // a row whose max then grows by more than 2^8 (lazy rescale below) redoes it.
+            // Bitwise identical to computing the max first.
+            const bool spec = kSpecMax && j > 0;
+            const float m_spec = m_run == -INFINITY ? 0.0f : m_run;
+            if (spec) quarter0(pa, m_spec);
+            // row max: tree of 3-input maxima, then (two halves) the other half's through smem
+            float mx = row_max<kC>(s);
+            if constexpr (kH == 2) {
+                xslot(j & 1, c)[r] = mx;
+                named_bar_sync(xbar, 256);  // also: every S column of the tile is in registers
+                mx = fmax_nr(mx, xslot(j & 1, c ^ 1)[r]);
+            }
+            bad |= !(mx < INFINITY);
+            const float m_tile = mx * sc;
+            if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE(2048 + 8 * j + 4 * t + 1);
+            if (j == 0) {
+                m_run = m_tile;
+            } else if (__any_sync(0xffffffffu, m_tile > m_run + 8.0f)) {
+                // Lazy rescale (warp-uniform: tcgen05.ld/st are .sync.aligned; both halves of
+                // a row see the same maxima, so they take the same branch).  The previous
+                // P V must have landed before O is touched.  Rows whose max did not grow
+                // enough keep their stale max (factor 1).
+                float f = 1.0f;
+                if (m_tile > m_run) {
+                    f = ex2(m_run - m_tile);
+                    m_run = m_tile;
+                }
+                l_run *= f;
+                o_wait();
+#pragma unroll kRescaleUnroll
+                for (int x = 0; x < kOC / 32; ++x) {
+                    uint32_t u[32];
+                    tmem_ld32(tO + 32 * x, u);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int y = 0; y < 32; ++y) u[y] = __float_as_uint(__uint_as_float(u[y]) * f);
+                    tmem_st32(tO + 32 * x, u);
+                }
+            }
+            const float m_use = m_run == -INFINITY ? 0.0f : m_run;
+            if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE(2048 + 8 * j + 4 * t + 2);
+            if (!spec || m_use != m_spec) {  // (per row: only rescaled rows redo)
+                ls2[0] = ls2[1] = make_float2(0.0f, 0.0f);
+                quarter0(pa, m_use);
+            }
             auto publish = [&](int qi) {  // quarter qi's tcgen05.st has been waited on
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full + 4 * t + kQ * c + qi);
                 if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE((qi < 3 ? 1024 + 1 + qi : 2048 + 3) + 8 * j + 4 * t);
             };
-            auto emit_row = [&](auto poly_pair) {
-                uint32_t pa[16], pb[16];
-                quarter(0, pa, poly_pair);
+            // The tensor-memory store of one quarter completes (wait::st) while the next is
+            // computed; the MMA warp starts P V on a quarter as soon as it lands.
+            auto emit_rest = [&](auto poly_pair) {
                 o_wait();  // (kSepP) P V(j-1) has read the P region
                 tmem_st16(tP + 0, pa);
 #pragma unroll
                 for (int qi = 1; qi < kQ; ++qi) {
-                    quarter(qi, (qi & 1) ? pb : pa, poly_pair);
+                    quarter(qi, (qi & 1) ? pb : pa, poly_pair, m_use);
                     tmem_wait_st();
                     publish(qi - 1);
                     tmem_st16(tP + 16 * qi, (qi & 1) ? pb : pa);
@@ -465,16 +502,10 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
                 tmem_wait_st();
                 publish(kQ - 1);
             };
-            constexpr int kPer = PolyPeriod<kD>::fwd;
-            auto poly_fast = [](int pair) {
-                if constexpr (kPer > 0) return pair % kPer == kPer - 1;
-                return false;
-            };
-            auto poly_none = [](int) { return false; };  // -inf -> exact 0 on masked tiles
-            if (tile_masked)  // warp-uniform: tcgen05.st is .sync.aligned
-                emit_row(poly_none);
+            if (kMaskedMufu && tile_masked)  // warp-uniform: tcgen05.st is .sync.aligned
+                emit_rest(poly_none);
             else
-                emit_row(poly_fast);
+                emit_rest(poly_fast);
             const float2 lsum = fadd2(ls2[0], ls2[1]);
             l_run += lsum.x + lsum.y;
         }
@@ -495,7 +526,7 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
                 if (p.status && (bad || !(l_tot > 0.0f))) atomicOr(p.status, 1u);
             }
             uint8_t* sO = sQ + t * Cfg::kTileBytes;  // Q_t is dead once the last S_t landed
-#pragma unroll
+#pragma unroll kRescaleUnroll
             for (int x = 0; x < kOC / 32; ++x) {
                 uint32_t u[32];
                 tmem_ld32(tO + 32 * x, u);

@@ -722,21 +722,23 @@ VATTN_DEV float ex2_poly(float x) {
 #define VATTN_POLY_DQ64 0
 #endif
 // dK/dV P pass: element pairs out of every 4 on the polynomial, per warpgroup (d = 128
-// and d = 64 knobs).  Asymmetric by design: both warpgroups exponentiate at the same
-// time, so moving half of ONE warpgroup's work to the FMA pipe lets the two finish
-// together (trace: -7 % per step for the heaviest C3 CTA; measured backward -2.2 % at
-// C3 / C5, -5 % at C2 N = 4k and C4).  Moving both warpgroups' work is 10 % slower.
+// and d = 64 knobs).  Round 1 chose an asymmetric 0 / 2 split (both warpgroups
+// exponentiate at the same time; -2.2 % vs 0 / 0 at C3).  Round 2: a symmetric 1 / 1
+// split is better still (dK/dV C3 -4 %, C2 / C4 d = 64 -3..-4 %; dQ recompute d = 64
+// -4..-6 %, profiles/r2_experiments.md) -- equal knobs compile ONE copy of the unrolled
+// P pass instead of one per warpgroup, and these kernels are sensitive to code size
+// (the forward's masked-tile copy measured the same way, -3..-5 %).
 #ifndef VATTN_POLY_DKDV_WG0
-#define VATTN_POLY_DKDV_WG0 0
+#define VATTN_POLY_DKDV_WG0 1
 #endif
 #ifndef VATTN_POLY_DKDV_WG1
-#define VATTN_POLY_DKDV_WG1 2
+#define VATTN_POLY_DKDV_WG1 1
 #endif
 #ifndef VATTN_POLY_DKDV64_WG0
-#define VATTN_POLY_DKDV64_WG0 0
+#define VATTN_POLY_DKDV64_WG0 1
 #endif
 #ifndef VATTN_POLY_DKDV64_WG1
-#define VATTN_POLY_DKDV64_WG1 2
+#define VATTN_POLY_DKDV64_WG1 1
 #endif
 // dQ recompute kernel P pass, same scheme (pairs out of every 4, per warpgroup)
 #ifndef VATTN_POLY_DQ_WG0
@@ -746,10 +748,10 @@ VATTN_DEV float ex2_poly(float x) {
 #define VATTN_POLY_DQ_WG1 0
 #endif
 #ifndef VATTN_POLY_DQ64_WG0
-#define VATTN_POLY_DQ64_WG0 0
+#define VATTN_POLY_DQ64_WG0 1
 #endif
 #ifndef VATTN_POLY_DQ64_WG1
-#define VATTN_POLY_DQ64_WG1 2
+#define VATTN_POLY_DQ64_WG1 1
 #endif
 template <int kD> struct PolyPeriod {
     static constexpr int fwd = kD == 64 ? VATTN_POLY_FWD64 : VATTN_POLY_FWD;
