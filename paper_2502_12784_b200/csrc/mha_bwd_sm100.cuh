@@ -282,7 +282,7 @@ VATTN_DEV void dq_worker(const CUtensorMap* tm_ds, const CUtensorMap* tm_k, cons
                     const uint64_t t0 = globaltimer_ns();
                     while (ld_acquire_gpu(cnt) < p.ds_signals) {
                         __nanosleep(500);
-                        if (globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) __trap();
+                        if (VATTN_WATCHDOG_NS && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) __trap();
                     }
                     fence_proxy_async_global();  // the TMA loads below see the dS^T stores
                 }

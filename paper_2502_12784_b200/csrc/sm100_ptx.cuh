@@ -187,7 +187,7 @@ VATTN_DEV void mbar_wait_mma_(uint64_t* bar, uint32_t parity) {
         __nanosleep(20);
 #endif
 #endif
-        if ((++n & 255u) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) __trap();
+        if (VATTN_WATCHDOG_NS && (++n & 255u) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) __trap();
     }
 }
 
@@ -440,7 +440,7 @@ VATTN_DEV void mbar_wait_mma_cl(uint64_t* bar, uint32_t parity) {
         const uint64_t t0 = globaltimer_ns();
         uint32_t n = 0;
         while (!mbar_try_wait_cl(bar, parity))
-            if ((++n & 255u) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) {
+            if (VATTN_WATCHDOG_NS && (++n & 255u) == 0 && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) {
 #ifdef VATTN_WATCHDOG_PRINT
                 printf("vattn watchdog (MMA, cluster): block %d stuck on mbarrier smem+0x%x parity %u\n", (int)blockIdx.x,
                        smem_u32(bar), parity);
