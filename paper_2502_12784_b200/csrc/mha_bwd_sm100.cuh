@@ -138,9 +138,9 @@ struct BwdParams {
 //   query-major  mask[unit][query][Npad/32]  bit = key    (forward, dQ recompute)
 //   key-major    mask[unit][key][Npad/32]    bit = query  (dK/dV: thread = key row)
 // CTA = one 128 x 128 (query tile, key tile) pair of one (b, h) unit; warp w hashes
-// queries 32 (w & 3) + lane against keys 64 (w >> 2) + [0, 64); 32 ballots per 32 x 32
-// block transpose the bits, staged in shared memory so both copies leave as 16-byte
-// stores.  Causal: tile pairs above the diagonal are skipped (masked positions; no
+// queries 32 (w & 3) + lane against keys 64 (w >> 2) + [0, 64) (drop_keep_word: the
+// hash with per-word constants); a five-stage shuffle transpose per 32 x 32 block makes
+// the key-major words, staged in shared memory so both copies leave as 16-byte stores.  Causal: tile pairs above the diagonal are skipped (masked positions; no
 // kernel reads their bits).
 __global__ void __launch_bounds__(256) mha_dropmask_kernel(uint32_t* __restrict__ mask, int Npad, int H, int bh_off,
                                                            uint64_t seed, uint64_t thresh, int causal, HashMul hm) {
@@ -167,28 +167,18 @@ __global__ void __launch_bounds__(256) mha_dropmask_kernel(uint32_t* __restrict_
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
         const int kw = kh * 2 + c;  // key word within the tile
-        uint32_t w = 0;
-        bool any_tie = false;
         const uint32_t col0 = static_cast<uint32_t>(j * 128 + kw * 32);
-#pragma unroll 8
-        for (int b = 0; b < 32; ++b) {
-            bool tie;
-            w |= static_cast<uint32_t>(drop_keep_mul(dr, col0 + b, th.hi, hm, tie)) << b;
-            any_tie |= tie;
-        }
-        if (any_tie) {  // a high word tied (p ~ 2^-32 per position): redo the word exactly
+        bool tie, wrap;
+        uint32_t w = th.hi < 0x80000000u ? drop_keep_word<true>(dr, col0, th.hi, tie, wrap)
+                                         : drop_keep_word<false>(dr, col0, th.hi, tie, wrap);
+        (void)hm;
+        if (tie || wrap) {  // a high word tied (p ~ 2^-32 per position) or K's low word wraps: exact
             w = 0;
 #pragma unroll 1
             for (int b = 0; b < 32; ++b) w |= static_cast<uint32_t>(drop_keep(dr, static_cast<int>(col0) + b, thresh)) << b;
         }
         qm[qs * 32 + lane][kw] = w;
-        uint32_t tw = 0;
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            const uint32_t col = __ballot_sync(0xffffffffu, (w >> b) & 1u);  // key kw*32+b, bit = query
-            if (lane == b) tw = col;
-        }
-        km[kw * 32 + lane][qs] = tw;
+        km[kw * 32 + lane][qs] = warp_transpose32(w, lane);  // key kw*32 + lane, bit = query
     }
     __syncthreads();
     const size_t base = static_cast<size_t>(bh) * Npad;

@@ -902,6 +902,8 @@ VATTN_DEV DropThresh drop_thresh_split(uint64_t thresh) {
 // (the caller redoes those positions exactly); otherwise returns the keep bit.
 struct HashMul {
     uint32_t m4, m32;  // 4 (>> 30, << 2), 32 (>> 27, << 5)
+    uint32_t one;      // 1: a * one + c64 as IMAD.WIDE (64-bit add with the carry in the high word)
+    uint32_t m2;       // 2 (>> 31)
 };
 VATTN_DEV bool drop_keep_mul(const DropRow& r, uint32_t col, uint32_t th_hi, const HashMul& m, bool& tie) {
     const uint64_t c = (r.s ^ (static_cast<uint64_t>(col) + r.k)) + 0x9e3779b97f4a7c15ull;
@@ -926,6 +928,66 @@ VATTN_DEV bool drop_keep_mul(const DropRow& r, uint32_t col, uint32_t th_hi, con
     tie = zh == th_hi;
     return zh > th_hi;
 }
+// 32 consecutive keys col0 .. col0 + 31 of one row at once (the mask kernel's word),
+// returning the keep bits (bit b = key col0 + b) and setting `tie` when any high word
+// tied (the caller then redoes the word exactly).  Per word, K = k + col0 keeps its high
+// word for all 32 keys (checked: the low word does not wrap; otherwise the exact path),
+// so the high word of x0 = (s ^ (K + b)) + G takes one of two values (carry of the low
+// add), and so do the high words of x0 ^ (x0 >> 30) and their product with C1's low
+// word: those are per-word constants selected by the carry.  Per key that leaves the
+// low-word add / xor, two funnel shifts, the two 32 x 32 partial products of x1 * C1, the
+// second xor-shift and the high word of x2 * C2 -- the same integers as drop_keep.
+// kLowThresh (th_hi < 2^31, i.e. p < 1/2): the final z ^= z >> 31 only flips bit 0 of
+// high words >= 2^31, which are above th_hi either way, so it is skipped.
+template <bool kLowThresh>
+VATTN_DEV uint32_t drop_keep_word(const DropRow& r, uint32_t col0, uint32_t th_hi, bool& tie, bool& wrap) {
+    constexpr uint32_t kGlo = 0x7f4a7c15u, kGhi = 0x9e3779b9u;
+    constexpr uint32_t kC1lo = 0x1ce4e5b9u, kC1hi = 0xbf58476du;
+    constexpr uint32_t kC2lo = 0x133111ebu, kC2hi = 0x94d049bbu;
+    const uint64_t K = r.k + col0;
+    const uint32_t Klo = static_cast<uint32_t>(K), Khi = static_cast<uint32_t>(K >> 32);
+    wrap = Klo > 0xFFFFFFFFu - 31u;
+    const uint32_t slo = static_cast<uint32_t>(r.s), shi = static_cast<uint32_t>(r.s >> 32);
+    const uint32_t xh = Khi ^ shi;
+    const uint32_t h0a = xh + kGhi, h0b = h0a + 1u;              // high word of x0 (carry 0 / 1)
+    const uint32_t h1a = h0a ^ (h0a >> 30), h1b = h0b ^ (h0b >> 30);  // high word of x1
+    const uint32_t hca = h1a * kC1lo, hcb = h1b * kC1lo;          // its share of hi(x1 * C1)
+    uint32_t w = 0;
+    bool t = false;
+#pragma unroll 8
+    for (uint32_t b = 0; b < 32; ++b) {
+        const uint32_t xl = (Klo + b) ^ slo;
+        const uint32_t lo0 = xl + kGlo;
+        const bool c = lo0 < kGlo;                                 // carry into the high word
+        const uint32_t hi0 = c ? h0b : h0a;
+        const uint32_t lo1 = lo0 ^ __funnelshift_r(lo0, hi0, 30);  // x ^= x >> 30 (low word)
+        const uint64_t pr = static_cast<uint64_t>(lo1) * kC1lo;
+        const uint32_t lo2 = static_cast<uint32_t>(pr);
+        const uint32_t hi2 = static_cast<uint32_t>(pr >> 32) + lo1 * kC1hi + (c ? hcb : hca);
+        const uint32_t lo3 = lo2 ^ __funnelshift_r(lo2, hi2, 27);  // x ^= x >> 27
+        const uint32_t hi3 = hi2 ^ (hi2 >> 27);
+        uint32_t zh = __umulhi(lo3, kC2lo) + lo3 * kC2hi + hi3 * kC2lo;  // high word of x * C2
+        if constexpr (!kLowThresh) zh ^= zh >> 31;
+        t |= zh == th_hi;
+        w |= static_cast<uint32_t>(zh > th_hi) << b;
+    }
+    tie = t;
+    return w;
+}
+
+// 32 x 32 bit transpose across a warp: lane l holds row l (bit c = column c) in, column l
+// (bit r = row r) out.  Five butterfly stages of shuffles (Hacker's Delight 7-3).
+VATTN_DEV uint32_t warp_transpose32(uint32_t x, int lane) {
+    uint32_t m = 0x0000FFFFu;
+#pragma unroll
+    for (int j = 16; j >= 1; j >>= 1) {
+        const uint32_t t = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~m) | ((t >> j) & m)) : ((x & m) | ((t & m) << j));
+        m ^= m << (j >> 1);
+    }
+    return x;
+}
+
 VATTN_DEV bool drop_keep_fast(const DropRow& r, int col, const DropThresh& th) {
     uint64_t x = (r.s ^ (static_cast<uint64_t>(col) + r.k)) + 0x9e3779b97f4a7c15ull;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
