@@ -342,6 +342,10 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
         float l_run = 0.0f;       // this half's row sum
         bool bad = false;         // a NaN or +inf score in this row (FMNMX.NAN keeps NaN in mx)
         const int ntile = t ? nk[1] : nk[0];
+        uint4 kw4_next = make_uint4(0u, 0u, 0u, 0u);
+        if (kDrop && p.drop_mask && row < p.mask_words * 32 && ntile > 0)
+            kw4_next = __ldg(reinterpret_cast<const uint4*>(p.drop_mask + (static_cast<size_t>(bh) * p.mask_words * 32 + row) *
+                                                                              p.mask_words));
         for (int j = 0; j < ntile; ++j) {
             mbar_wait<VATTN_SLEEP_MATH>(s_full + t, j & 1);
             // O += P V of the previous tile has landed (issued before S(j), so this wait
@@ -361,10 +365,12 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
             };
             stress_delay(1, j);
             if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE(1024 + 8 * j + 4 * t + 0);
-            uint4 kw4 = make_uint4(0u, 0u, 0u, 0u);  // this row's keep bits of key tile j
-            if (kDrop && p.drop_mask && row < p.mask_words * 32)
-                kw4 = __ldg(reinterpret_cast<const uint4*>(p.drop_mask + (static_cast<size_t>(bh) * p.mask_words * 32 + row) *
-                                                                             p.mask_words + j * 4));
+            // this row's keep bits of key tile j, loaded one step ahead (the mask streams
+            // from HBM: its latency stays off the softmax)
+            const uint4 kw4 = kw4_next;
+            if (kDrop && p.drop_mask && row < p.mask_words * 32 && j + 1 < ntile)
+                kw4_next = __ldg(reinterpret_cast<const uint4*>(p.drop_mask + (static_cast<size_t>(bh) * p.mask_words * 32 + row) *
+                                                                                  p.mask_words + (j + 1) * 4));
             float s[kC];
 #pragma unroll
             for (int x = 0; x < kC / 32; ++x) tmem_ld32f(tS + 32 * x, s + 32 * x);
