@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             mbar_wait(s_full + (kDB ? (s & 1) : 0), kDB ? ((s >> 1) & 1) : (s & 1));
             tc_fence_after();
             stress_delay(1, s);
-            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 0);
+            if ((warp == 4 || warp == 8) && lane == 0) VTRACE(1024 + 8 * s + 0 + (warp == 8 ? 4 : 0));
             float pr[kQW];
 #pragma unroll
             for (int c = 0; c < kCh; ++c) tmem_ld32f(tmem + lb + sR + kQW * h + 32 * c, pr + 32 * c);
@@ -871,12 +871,12 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                 p_pass(std::integral_constant<int, kPoly0>{});
             else
                 p_pass(std::integral_constant<int, kPoly1>{});
-            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 1);
+            if ((warp == 4 || warp == 8) && lane == 0) VTRACE(1024 + 8 * s + 1 + (warp == 8 ? 4 : 0));
             stress_delay(2, s);
 
             mbar_wait(dp_full, s & 1);
             tc_fence_after();
-            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 2);
+            if ((warp == 4 || warp == 8) && lane == 0) VTRACE(1024 + 8 * s + 2 + (warp == 8 ? 4 : 0));
             uint32_t dsp[kQW / 2];
 #pragma unroll
             for (int c = 0; c < kCh; ++c) {
@@ -946,7 +946,7 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                 }
             }
 
-            if (warp == 4 && lane == 0) VTRACE(1024 + 8 * s + 3);
+            if ((warp == 4 || warp == 8) && lane == 0) VTRACE(1024 + 8 * s + 3 + (warp == 8 ? 4 : 0));
         }
         if (p.ds_out && (warp & 3) == 0 && lane == 0) {
             if (p.dq_sync) {  // this CTA's dS^T stores are in memory: count them for the dQ workers

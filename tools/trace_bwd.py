@@ -89,7 +89,7 @@ if "dq" not in sys.argv:
         print(f"{it:3d} | " + " ".join(f"{x:7d}" for x in m) + " | " + " | ".join(rows) + f" | {dtv}")
     print(f"== dK/dV, block {block}")
     t = trace(1, bwd)
-    show(t, ["p_full", "S_next", "ds_full"], ["s_full", "P_done", "dp_full", "dS_done"], min(n_q, 24), 8)
+    show(t, ["p_full", "S_next", "ds_full"], ["s_full", "P_done", "dp_full", "dS_done", "s_full1", "P_done1", "dp_full1", "dS_done1"], min(n_q, 24), 8)
 print(f"== dQ, block {block}")
 t = trace(2, bwd)
 show(t, ["ds_full", "v_next", "k_next2", "dQ_iss", "commit", "dP_iss", "S_iss"], ["s_full", "P_done", "dp_full", "dS_done"], min(n_q, 24), 8)
