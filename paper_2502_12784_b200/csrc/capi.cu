@@ -643,14 +643,23 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
                    L.materialize_ds ? mds : mq, mq, mdo, mdq, dk, dv, p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)
-    if (W > 0) {  // what the overlapped workers left: full width
+    // The dQ GEMM runs as the persistent worker kernel (one CTA per SM looping over the
+    // (unit, query tile) items; bitwise the same as one CTA per tile): C2 N = 512 / 1k and
+    // C4 steps -3 / -1 / -1 %, C3 neutral.  VATTN_DQ_PERSIST=0: one CTA per query tile.
+    static const bool persist_env = [] {
+        const char* e = getenv("VATTN_DQ_PERSIST");
+        return !(e && atoi(e) == 0);
+    }();
+    if (W > 0 || (persist_env && L.materialize_ds && !pair)) {  // full width (after the workers, if any)
         auto kern = mha_bwd_dq_tail_kernel<kD, kBF16>;
         constexpr int smem = DqGemmCfg<kD>::kSmemBytes;
         const cudaError_t ae = set_smem_once<mha_bwd_dq_tail_kernel<kD, kBF16>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 2);
         const int items = L.n_q * BH;
-        launch_pdl(kern, dim3(items < sms ? items : sms), dim3(256), smem, stream, mds, mk, mdq, p);
+        BwdParams pt = p;
+        pt.dq_sync = reinterpret_cast<int*>(w + L.sync);  // [0]: the item counter
+        launch_pdl(kern, dim3(items < sms ? items : sms), dim3(256), smem, stream, mds, mk, mdq, pt);
     } else if (L.materialize_ds) {
         auto kern = mha_bwd_dq_gemm_kernel<kD, kBF16>;
         constexpr int smem = DqGemmCfg<kD>::kSmemBytes;

@@ -299,22 +299,26 @@ for (B, H, N, d, causal, dtype) in [(1, 2, 384, 128, True, torch.bfloat16), (2, 
     dq, dk, dv = vb.mha_backward(q, k, v, o, do, lse, causal)
     rdq, rdk, rdv = po.attention_grad_ref(widen(q), widen(k), widen(v), widen(do), causal)
     for name, t, r in (("dQ", dq, rdq), ("dK", dk, rdk), ("dV", dv, rdv)):
-        check_close(widen(t), r, dtype, name + " mode " + os.environ["VATTN_DQ_MODE"])
+        check_close(widen(t), r, dtype, name + " mode " + os.environ["VATTN_DQ_MODE"] + " persist " + os.environ.get("VATTN_DQ_PERSIST", "1"))
     a = vb.mha_backward(q, k, v, o, do, lse, causal)
     assert all(torch.equal(x, y) for x, y in zip((dq, dk, dv), a)), "not deterministic"
 print("OK")
 '''
 
 
-@pytest.mark.parametrize("mode", ["0", "1"])
+@pytest.mark.parametrize("mode", ["0", "1", "1-per-tile"])
 def test_dq_modes_vs_binary64(mode):
-    """dQ by recompute (mode 0, mha_bwd_dq_kernel) and from materialised dS (mode 1,
-    mha_bwd_dq_gemm_kernel) both meet the binary64 tolerances and are deterministic.
-    The mode is read once per process, hence the subprocess."""
+    """dQ by recompute (mode 0, mha_bwd_dq_kernel) and from materialised dS (mode 1: the
+    persistent mha_bwd_dq_tail_kernel by default, mha_bwd_dq_gemm_kernel -- one CTA per
+    query tile -- with VATTN_DQ_PERSIST=0) all meet the binary64 tolerances and are
+    deterministic.  The modes are read once per process, hence the subprocess."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _DQ_MODE_CHILD], env=dict(os.environ, VATTN_DQ_MODE=mode, ROOT=root),
+    env = dict(os.environ, VATTN_DQ_MODE=mode[0], ROOT=root)
+    if mode.endswith("per-tile"):
+        env["VATTN_DQ_PERSIST"] = "0"
+    r = subprocess.run([sys.executable, "-c", _DQ_MODE_CHILD], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
