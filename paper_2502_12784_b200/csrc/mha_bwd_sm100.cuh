@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(256) mha_bwd_preprocess_kernel(
     const void* __restrict__ o, const void* __restrict__ dout, const float* __restrict__ lse,
     float* __restrict__ lse2, float* __restrict__ dsum, int N, int Npad, int BH, int* __restrict__ zero = nullptr,
     int zero_n = 0) {
+    griddep_start();
     using T16 = typename std::conditional<kBF16, __nv_bfloat16, __half>::type;
     constexpr int kLanesPerRow = kD / 8;
     constexpr int kRowsPerWarp = 32 / kLanesPerRow;
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(256) mha_bwd_preprocess_kernel(
             }
         }
     }
-    griddep_launch_dependents();
+    if (!kPdlEarly) griddep_launch_dependents();
 }
 
 struct BwdParams {
@@ -144,6 +145,7 @@ struct BwdParams {
 // kernel reads their bits).
 __global__ void __launch_bounds__(256) mha_dropmask_kernel(uint32_t* __restrict__ mask, int Npad, int H, int bh_off,
                                                            uint64_t seed, uint64_t thresh, int causal, HashMul hm) {
+    griddep_start();
     __shared__ uint32_t qm[128][5];  // [query][key word] (+1 pad)
     __shared__ uint32_t km[128][5];  // [key][query word]
     const int nt = Npad / 128, W = Npad / 32;
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(256) mha_dropmask_kernel(uint32_t* __restrict_
         *reinterpret_cast<uint4*>(mask + half + (base + j * 128 + r) * W + i * 4) =
             make_uint4(km[r][0], km[r][1], km[r][2], km[r][3]);
     }
-    griddep_launch_dependents();
+    if (!kPdlEarly) griddep_launch_dependents();
 }
 
 // Index of dS^T tile (query tile i, key tile kb) within one (b, h).
@@ -357,7 +359,7 @@ VATTN_DEV void dq_worker(const CUtensorMap* tm_ds, const CUtensorMap* tm_k, cons
         tc_fence_after();
     }
     if (warp == 4 && lane == 0) bulk_wait_read0();  // no store reads smem past exit
-    griddep_launch_dependents();
+    if (!kPdlEarly) griddep_launch_dependents();
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -371,6 +373,7 @@ template <int kD, bool kBF16>
 __global__ void __launch_bounds__(256, 1)
     mha_bwd_dq_tail_kernel(const __grid_constant__ CUtensorMap tm_ds, const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
+    griddep_start();
     extern __shared__ __align__(1024) uint8_t smem[];
     dq_worker<kD, kBF16>(&tm_ds, &tm_k, &tm_dq, p, smem, false);
 }
@@ -460,6 +463,7 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                         const __grid_constant__ CUtensorMap tm_dq,    // dQ (dq_workers > 0)
                         void* __restrict__ dk_out, void* __restrict__ dv_out, const BwdParams p) {
     VCTA(1, 0);
+    griddep_start();
     using Cfg = DkdvCfg<kD>;
     static_assert(!kPair || (kD == 128 && !Cfg::kDoubleS), "CTA pair: d = 128 only");
     if constexpr (!kPair) {  // the grid's first dq_workers CTAs overlap the dQ GEMM (see dq_worker)
@@ -1001,7 +1005,7 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             }
         }
     }
-    griddep_launch_dependents();
+    if (!kPdlEarly) griddep_launch_dependents();
     tc_fence_before();
     if constexpr (!kPair) {
         if (p.dq_sync) {  // after this CTA's dS^T counts (the barrier below orders them)
@@ -1066,6 +1070,7 @@ __global__ void __launch_bounds__(384, 1)
                       const __grid_constant__ CUtensorMap tm_do,
                       const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
     VCTA(2, 0);
+    griddep_start();
     using Cfg = DqCfg<kD>;
     constexpr int kVtraceKid = 2;
     (void)kVtraceKid;
@@ -1392,7 +1397,7 @@ __global__ void __launch_bounds__(384, 1)
             bulk_wait_read0();
         }
     }
-    griddep_launch_dependents();
+    if (!kPdlEarly) griddep_launch_dependents();
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -1415,6 +1420,7 @@ __global__ void __launch_bounds__(256, 1)
     mha_bwd_dq_gemm_kernel(const __grid_constant__ CUtensorMap tm_ds, const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
     VCTA(3, 0);
+    griddep_start();
     using Cfg = DqGemmCfg<kD>;
     constexpr int S = Cfg::kStages;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -1512,7 +1518,7 @@ __global__ void __launch_bounds__(256, 1)
             bulk_wait_read0();
         }
     }
-    griddep_launch_dependents();
+    if (!kPdlEarly) griddep_launch_dependents();
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {

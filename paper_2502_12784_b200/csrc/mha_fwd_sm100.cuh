@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
                          const __grid_constant__ CUtensorMap tm_v,
                          const __grid_constant__ CUtensorMap tm_o, const FwdParams p) {
     VCTA(0, 0);
+    griddep_start();
     using Cfg = FwdCfg<kD>;
     constexpr int kVtraceKid = 0;
     (void)kVtraceKid;
@@ -558,7 +559,7 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
             }
         }
     }
-    griddep_launch_dependents();
+    if (!kPdlEarly) griddep_launch_dependents();
     tc_fence_before();
     __syncthreads();
     if (warp == Cfg::kAllocWarp) {
