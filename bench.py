@@ -509,7 +509,8 @@ def main():
             "fwd_tflops": f_fwd / (fwd_ms * 1e-3) / 1e12,
             "bwd_tflops": f_bwd / ((pre_ms + dkdv_ms + dq_ms) * 1e-3) / 1e12,
             "bwd_dq_mode": dq_mode,
-            "dq_kernel": ({"kernel": "mha_bwd_dq_gemm_kernel", "bound": "hbm",
+            "dq_kernel": ({"kernel": ("mha_bwd_dq_gemm_kernel" if os.environ.get("VATTN_DQ_PERSIST") == "0"
+                                      else "mha_bwd_dq_tail_kernel (persistent dQ GEMM)"), "bound": "hbm",
                            "achieved_gbs": ds_bytes / (dq_ms * 1e-3) / 1e9,
                            "bytes_note": "dS^T tiles streamed once (16-bit, 32 KiB per tile pair)"}
                           if dq_mode == "dS-GEMM" else

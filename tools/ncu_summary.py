@@ -46,6 +46,7 @@ SHORT = {
     "mha_bwd_dkdv_kernel": "bwd_dkdv",
     "mha_bwd_dq_kernel": "bwd_dq",
     "mha_bwd_dq_gemm_kernel": "bwd_dq_gemm",
+    "mha_bwd_dq_tail_kernel": "bwd_dq_gemm",  # the persistent dQ GEMM (same role)
     "mha_bwd_preprocess_kernel": "bwd_preprocess",
 }
 
