@@ -4,6 +4,7 @@ explicit softmax scales) through the reference-shaped API (`forward_fused` /
 `backward_fused`, which zero-pads head dims other than 64 / 128) against the binary64
 oracle with the SURVEY 8(c) tolerances, plus bitwise run-to-run determinism.  The
 fixed seed list keeps every case reproducible by its id."""
+import os
 import random
 
 import numpy as np
@@ -34,6 +35,10 @@ def _case(seed):
 
 
 SEEDS = list(range(100, 124))
+# VATTN_FUZZ_SEEDS=a:b widens the sweep for a one-off soak (tools/gpu_fuzz.sh)
+if os.environ.get("VATTN_FUZZ_SEEDS"):
+    _a, _b = (int(x) for x in os.environ["VATTN_FUZZ_SEEDS"].split(":"))
+    SEEDS = list(range(_a, _b))
 
 
 @pytest.mark.parametrize("seed", SEEDS, ids=[f"s{s}" for s in SEEDS])
