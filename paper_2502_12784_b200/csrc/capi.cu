@@ -596,6 +596,20 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     p.dkdv_ctas = L.n_q * BH;
     p.n_units = BH;
     p.ds_signals = DkdvCfg<kD>::kWG * L.n_q;
+    p.dkdv_items = L.n_q * BH;
+    // Persistent dK/dV (one CTA per SM looping over the (unit, key tile) items, static
+    // round robin; the next item's K / V / Q / dO loads and first S / dP MMAs overlap the
+    // current item's epilogue) for short heads, N <= 1024: C2 N = 512 -10 %, N = 1k -7 %,
+    // C4 -3.4 % per step.  At long causal N the static assignment loses the longest-first
+    // balance of one CTA per item (C3 +7.5 %), so those keep one CTA per item.
+    // VATTN_DKDV_PERSIST=0 / 1 forces either.  Not with the overlapped dQ workers, which
+    // count finished items per CTA.
+    static const int dkdv_persist_env = [] {
+        const char* e = getenv("VATTN_DKDV_PERSIST");
+        return e ? atoi(e) : -1;
+    }();
+    const bool dkdv_persist = dkdv_persist_env >= 0 ? dkdv_persist_env == 1 : L.n_q <= 8;
+    const int dkdv_ctas = (dkdv_persist && W == 0 && p.dkdv_items > sms) ? sms : p.dkdv_items;
     p.tail_units = c->causal ? (pair ? dkdv_tail_units(BH, n_pairs, 2) : dkdv_tail_units(BH, L.n_q)) : 0;
     p.drop_mask = nullptr;
     p.drop_mask_k = nullptr;
@@ -639,7 +653,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
-        launch_pdl(kern, dim3(L.n_q * BH + W), dim3(DkdvCfg<kD>::kThreads), smem, stream, mq, mk, mv, mdo,
+        launch_pdl(kern, dim3(dkdv_ctas + W), dim3(DkdvCfg<kD>::kThreads), smem, stream, mq, mk, mv, mdo,
                    L.materialize_ds ? mds : mq, mq, mdo, mdq, dk, dv, p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)

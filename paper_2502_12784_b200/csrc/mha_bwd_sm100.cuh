@@ -130,6 +130,8 @@ struct BwdParams {
     int dkdv_ctas;
     int n_units;        // (b, h) units of this launch
     int ds_signals;     // dS^T store-done signals per unit (store threads per key tile x n_q)
+    int dkdv_items;     // (unit, key tile) items of the dK/dV grid; a CTA takes items
+                        // cta, cta + G, ... (G = its CTAs) -- persistent when G < items
 };
 
 // Dropout keep bits, hashed once per step ahead of the forward: the reference's
@@ -434,7 +436,7 @@ struct DkdvCfg {
     // kv_full, q_full/q_empty [kStages], s_full (x2 double S), dp_full, p_full, ds_full,
     // dkv_full, ld_full [kStages] (CTA pair: lse2 / D of this CTA; Q / dO count on the
     // leader's q_full)
-    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 1 + 2 * kWG * kHalves + kWG + 1 + kStages;
+    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 1 + 2 * kWG * kHalves + kWG + 1 + kStages + 1;  // + acc_free
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr uint32_t kTmemS = 0;                       // region r at 128 r
     static constexpr uint32_t kTmemDP = kDoubleS ? 256 : 128;
@@ -508,27 +510,40 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
     // lse2 / D of a stage: the CTA pair's own barrier (its Q / dO bytes count on the
     // leader's q_full); one CTA: part of q_full
     uint64_t* ld_full = kPair ? dkv_full + 1 : q_full;  // [kSt]
+    // persistent CTAs: the epilogue has read dV / dK out of tensor memory (the next item's
+    // first dV / dK MMAs overwrite them)
+    uint64_t* acc_free = dkv_full + 1 + kSt;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
     const int warp = warp_id();
     const int lane = lane_id();
     const uint32_t rank = kPair ? cluster_rank() : 0u;  // 0 = leader (issues the MMAs)
-    // causal: the key tiles with the most query tiles first
-    int bh, kb;
-    if constexpr (kPair) {  // cluster c = key tiles (2 pr, 2 pr + 1) of unit bh
-        int pr;
-        grid_item_tail_n(static_cast<int>(blockIdx.x >> 1), static_cast<int>(gridDim.x >> 1), (p.n_q + 1) >> 1,
-                         p.tail_units, bh, pr);
-        kb = 2 * pr + static_cast<int>(rank);
-    } else {
-        grid_item_tail_n(static_cast<int>(blockIdx.x) - p.dq_workers, static_cast<int>(gridDim.x) - p.dq_workers, p.n_q,
-                         p.tail_units, bh, kb);
-    }
+    // Items: (unit, key tile), in the dispatch order of grid_item_tail (causal: the key
+    // tiles with the most query tiles first); CTA c takes items c, c + G, c + 2G, ...
     const int N = p.N;
-    // causal: both CTAs of a pair start at the lower key tile's diagonal (the upper
-    // tile's first query tile is fully masked)
-    const int i0 = p.causal ? (kPair ? (kb & ~1) : kb) : 0;
-    const int n_steps = p.n_q - i0;
+    const int cta = static_cast<int>(blockIdx.x) - p.dq_workers;
+    const int G = static_cast<int>(gridDim.x) - p.dq_workers;
+    struct Item {
+        int bh, kb, i0, n_steps;
+    };
+    auto item_at = [&](int it, Item& x) -> bool {
+        if constexpr (kPair) {  // cluster c = key tiles (2 pr, 2 pr + 1) of unit bh; one item per cluster
+            if (it > 0) return false;
+            int pr;
+            grid_item_tail_n(static_cast<int>(blockIdx.x >> 1), static_cast<int>(gridDim.x >> 1), (p.n_q + 1) >> 1,
+                             p.tail_units, x.bh, pr);
+            x.kb = 2 * pr + static_cast<int>(rank);
+        } else {
+            const int L = cta + it * G;
+            if (L >= p.dkdv_items) return false;
+            grid_item_tail_n(L, p.dkdv_items, p.n_q, p.tail_units, x.bh, x.kb);
+        }
+        // causal: both CTAs of a pair start at the lower key tile's diagonal (the upper
+        // tile's first query tile is fully masked)
+        x.i0 = p.causal ? (kPair ? (x.kb & ~1) : x.kb) : 0;
+        x.n_steps = p.n_q - x.i0;
+        return true;
+    };
     // a math warp's arrival on a barrier the MMA issuer waits on (the leader's for a pair)
     auto arrive_mma = [&](uint64_t* bar) {
         if constexpr (kPair)
@@ -553,6 +568,7 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
         mbar_init(dkv_full, 1);
         if (kPair)
             for (int s = 0; s < kSt; ++s) mbar_init(ld_full + s, 1);
+        mbar_init(acc_free, 4 * kWG);  // one arrive per math warp
         fence_barrier_init();
     }
     if constexpr (kPair) {
@@ -579,49 +595,59 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             if constexpr (kPair) {
                 tma_prefetch_desc(&tm_q64);
                 tma_prefetch_desc(&tm_do64);
-                // K, V of both CTAs count on the leader's kv_full
-                const uint32_t kv_cl = mapa_u32(kv_full, 0);
-                if (rank == 0) mbar_arrive_expect_tx(kv_full, 4 * Cfg::kTileBytes);
-                for (int b = 0; b < Cfg::kBoxes; ++b) {
-                    tma_load_3d_pair(sK + b * 16384, &tm_k, kv_cl, b * 64, kb * 128, bh);
-                    tma_load_3d_pair(sV + b * 16384, &tm_v, kv_cl, b * 64, kb * 128, bh);
-                }
-            } else {
-                mbar_arrive_expect_tx(kv_full, 2 * Cfg::kTileBytes);
-                for (int b = 0; b < Cfg::kBoxes; ++b) {
-                    tma_load_3d(sK + b * 16384, &tm_k, kv_full, b * 64, kb * 128, bh);
-                    tma_load_3d(sV + b * 16384, &tm_v, kv_full, b * 64, kb * 128, bh);
-                }
             }
-            for (int s = 0; s < n_steps; ++s) {
-                const int st = s % kSt;
-                const int i = i0 + s;
-                stress_delay(4, s);
-                mbar_wait(q_empty + st, ((s / kSt) & 1) ^ 1);
-                uint8_t* q_st = sQ + st * Cfg::kTileBytes;
-                uint8_t* do_st = sDO + st * Cfg::kTileBytes;
+            uint32_t g0 = 0;  // steps of this CTA's earlier items (ring position)
+            Item x;
+            for (int it = 0; item_at(it, x); ++it) {
+                const int bh = x.bh, kb = x.kb;
+                if (it > 0) mbar_wait(dkv_full, (it - 1) & 1);  // the previous item's MMAs are done with K / V
                 if constexpr (kPair) {
-                    // [all 128 queries x d-half r] then [queries 64r.. +64 x d 0..127] (2 boxes)
-                    const uint32_t q_cl = mapa_u32(q_full + st, 0);
-                    if (rank == 0) mbar_arrive_expect_tx(q_full + st, 4 * Cfg::kTileBytes);
-                    const int r64 = static_cast<int>(rank) * 64;
-                    tma_load_3d_pair(q_st, &tm_q, q_cl, r64, i * 128, bh);
-                    tma_load_3d_pair(do_st, &tm_do, q_cl, r64, i * 128, bh);
-                    for (int b = 0; b < 2; ++b) {
-                        tma_load_3d_pair(q_st + 16384 + b * 8192, &tm_q64, q_cl, b * 64, i * 128 + r64, bh);
-                        tma_load_3d_pair(do_st + 16384 + b * 8192, &tm_do64, q_cl, b * 64, i * 128 + r64, bh);
-                    }
-                    mbar_arrive_expect_tx(ld_full + st, 1024);
-                } else {
-                    mbar_arrive_expect_tx(q_full + st, 2 * Cfg::kTileBytes + 1024);
+                    // K, V of both CTAs count on the leader's kv_full
+                    const uint32_t kv_cl = mapa_u32(kv_full, 0);
+                    if (rank == 0) mbar_arrive_expect_tx(kv_full, 4 * Cfg::kTileBytes);
                     for (int b = 0; b < Cfg::kBoxes; ++b) {
-                        tma_load_3d(q_st + b * 16384, &tm_q, q_full + st, b * 64, i * 128, bh);
-                        tma_load_3d(do_st + b * 16384, &tm_do, q_full + st, b * 64, i * 128, bh);
+                        tma_load_3d_pair(sK + b * 16384, &tm_k, kv_cl, b * 64, kb * 128, bh);
+                        tma_load_3d_pair(sV + b * 16384, &tm_v, kv_cl, b * 64, kb * 128, bh);
+                    }
+                } else {
+                    mbar_arrive_expect_tx(kv_full, 2 * Cfg::kTileBytes);
+                    for (int b = 0; b < Cfg::kBoxes; ++b) {
+                        tma_load_3d(sK + b * 16384, &tm_k, kv_full, b * 64, kb * 128, bh);
+                        tma_load_3d(sV + b * 16384, &tm_v, kv_full, b * 64, kb * 128, bh);
                     }
                 }
-                const size_t ro = static_cast<size_t>(bh) * p.Npad + static_cast<size_t>(i) * 128;
-                bulk_load(sLD + st * 256, p.lse2 + ro, 512, ld_full + st);
-                bulk_load(sLD + st * 256 + 128, p.dsum + ro, 512, ld_full + st);
+                for (int s = 0; s < x.n_steps; ++s) {
+                    const uint32_t g = g0 + s;
+                    const int st = g % kSt;
+                    const int i = x.i0 + s;
+                    stress_delay(4, s);
+                    mbar_wait(q_empty + st, ((g / kSt) & 1) ^ 1);
+                    uint8_t* q_st = sQ + st * Cfg::kTileBytes;
+                    uint8_t* do_st = sDO + st * Cfg::kTileBytes;
+                    if constexpr (kPair) {
+                        // [all 128 queries x d-half r] then [queries 64r.. +64 x d 0..127] (2 boxes)
+                        const uint32_t q_cl = mapa_u32(q_full + st, 0);
+                        if (rank == 0) mbar_arrive_expect_tx(q_full + st, 4 * Cfg::kTileBytes);
+                        const int r64 = static_cast<int>(rank) * 64;
+                        tma_load_3d_pair(q_st, &tm_q, q_cl, r64, i * 128, bh);
+                        tma_load_3d_pair(do_st, &tm_do, q_cl, r64, i * 128, bh);
+                        for (int b = 0; b < 2; ++b) {
+                            tma_load_3d_pair(q_st + 16384 + b * 8192, &tm_q64, q_cl, b * 64, i * 128 + r64, bh);
+                            tma_load_3d_pair(do_st + 16384 + b * 8192, &tm_do64, q_cl, b * 64, i * 128 + r64, bh);
+                        }
+                        mbar_arrive_expect_tx(ld_full + st, 1024);
+                    } else {
+                        mbar_arrive_expect_tx(q_full + st, 2 * Cfg::kTileBytes + 1024);
+                        for (int b = 0; b < Cfg::kBoxes; ++b) {
+                            tma_load_3d(q_st + b * 16384, &tm_q, q_full + st, b * 64, i * 128, bh);
+                            tma_load_3d(do_st + b * 16384, &tm_do, q_full + st, b * 64, i * 128, bh);
+                        }
+                    }
+                    const size_t ro = static_cast<size_t>(bh) * p.Npad + static_cast<size_t>(i) * 128;
+                    bulk_load(sLD + st * 256, p.lse2 + ro, 512, ld_full + st);
+                    bulk_load(sLD + st * 256 + 128, p.dsum + ro, 512, ld_full + st);
+                }
+                g0 += x.n_steps;
             }
         }
     } else if (warp == 1 && (!kPair || rank == 0)) {
@@ -679,75 +705,98 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                     mma_ts_e(tmem + dcol, a_col, desc_mnmajor(bd, kk), idesc_kmn, (acc || kk > 0) ? 1u : 0u);
             }
         };
-        mbar_wait(kv_full, 0);
-        tc_fence_after();
-        mbar_wait(q_full + 0, 0);
-        tc_fence_after();
-        issue_kk(Cfg::kTmemS, dK, dQk);
-        mma_commit_e(s_full);
-        issue_kk(Cfg::kTmemDP, dV, dDOk);
-        mma_commit_e(dp_full);
-        VTRACE(3072);
-        if constexpr (kDB) {
-            if (n_steps > 1) {
-                mbar_wait_mma(q_full + 1, 0);
-                tc_fence_after();
-                issue_kk(Cfg::kTmemS + 128, dK, dQk + kTile16);  // S_1 into the second region
-                mma_commit_e(s_full + 1);
-            }
+        uint32_t g0 = 0;  // steps of this CTA's earlier items
+        Item x;
+        for (int it = 0; item_at(it, x); ++it) {
+            const int n_steps = x.n_steps;
+            const uint32_t R0 = kDB ? (g0 & 1u) * 128u : 0u;  // S region of the item's first step
+            mbar_wait_mma(kv_full, it & 1);
+            tc_fence_after();
+            mbar_wait_mma(q_full + g0 % kSt, (g0 / kSt) & 1);
+            tc_fence_after();
+            issue_kk(Cfg::kTmemS + R0, dK, dQk + (g0 % kSt) * kTile16);
+            mma_commit_e(s_full + (kDB ? (g0 & 1u) : 0u));
+            issue_kk(Cfg::kTmemDP, dV, dDOk + (g0 % kSt) * kTile16);
+            mma_commit_e(dp_full);
+            VTRACE(3072);
+            // the previous item's epilogue has read dV / dK out of tensor memory
+            auto acc_wait = [&](int s) {
+                if (it > 0 && s == 0) {
+                    mbar_wait_mma(acc_free, (it - 1) & 1);
+                    tc_fence_after();
+                }
+            };
+            if constexpr (kDB) {
+                if (n_steps > 1) {
+                    const uint32_t g1 = g0 + 1;
+                    mbar_wait_mma(q_full + g1 % kSt, (g1 / kSt) & 1);
+                    tc_fence_after();
+                    issue_kk(Cfg::kTmemS + (g1 & 1u) * 128u, dK, dQk + (g1 % kSt) * kTile16);  // S_1: the other region
+                    mma_commit_e(s_full + (g1 & 1u));
+                }
+                for (int s = 0; s < n_steps; ++s) {
+                    const uint32_t g = g0 + s;
+                    const int st = g % kSt, st1 = (g + 1) % kSt, st2 = (g + 2) % kSt;
+                    const uint32_t R = (g & 1u) * 128u;
+                    stress_delay(3, s);
+                    acc_wait(s);
+                    issue_ts(Cfg::kTmemDV, Cfg::kTmemS + R, dDOm + st * kTile16, s > 0, p_full + kWG * kHv * (g & 1u),
+                             (g >> 1) & 1, std::true_type{});  // dV += P^T dO
+                    issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, g & 1, std::false_type{});  // dK += dS^T Q
+                    mma_commit_e(q_empty + st);
+                    if (s + 1 < n_steps) {
+                        issue_kk(Cfg::kTmemDP, dV, dDOk + st1 * kTile16);  // after dK read dS^T
+                        mma_commit_e(dp_full);
+                    }
+                    if (s + 2 < n_steps) {  // region R is free once dV_s read P^T_s (in order)
+                        mbar_wait_mma(q_full + st2, ((g + 2) / kSt) & 1);
+                        tc_fence_after();
+                        issue_kk(Cfg::kTmemS + R, dK, dQk + st2 * kTile16);
+                        mma_commit_e(s_full + (g & 1u));
+                    }
+                }
+            } else
             for (int s = 0; s < n_steps; ++s) {
-                const int st = s % kSt, st1 = (s + 1) % kSt, st2 = (s + 2) % kSt;
-                const uint32_t R = (s & 1) * 128u;
+                const uint32_t g = g0 + s;
+                const int st = g % kSt;
+                const int st1 = (g + 1) % kSt;
                 stress_delay(3, s);
-                issue_ts(Cfg::kTmemDV, Cfg::kTmemS + R, dDOm + st * kTile16, s > 0, p_full + kWG * kHv * (s & 1), (s >> 1) & 1,
+                acc_wait(s);
+                issue_ts(Cfg::kTmemDV, Cfg::kTmemS, dDOm + st * kTile16, s > 0, p_full + kWG * kHv * (g & 1u), (g >> 1) & 1,
                          std::true_type{});  // dV += P^T dO
-                issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, s & 1, std::false_type{});  // dK += dS^T Q
+                VTRACE(8 * s + 0);
+                if (s + 1 < n_steps) {
+                    mbar_wait(q_full + st1, ((g + 1) / kSt) & 1);
+                    tc_fence_after();
+                    VTRACE(8 * s + 1);
+                    issue_kk(Cfg::kTmemS, dK, dQk + st1 * kTile16);  // in-order after dV read P^T
+                    mma_commit_e(s_full);
+                }
+                issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, g & 1, std::false_type{});  // dK += dS^T Q
+                VTRACE(8 * s + 2);
                 mma_commit_e(q_empty + st);
                 if (s + 1 < n_steps) {
                     issue_kk(Cfg::kTmemDP, dV, dDOk + st1 * kTile16);  // after dK read dS^T
                     mma_commit_e(dp_full);
                 }
-                if (s + 2 < n_steps) {  // region R is free once dV_s read P^T_s (in order)
-                    mbar_wait_mma(q_full + st2, ((s + 2) / kSt) & 1);
-                    tc_fence_after();
-                    issue_kk(Cfg::kTmemS + R, dK, dQk + st2 * kTile16);
-                    mma_commit_e(s_full + (s & 1));
-                }
             }
-        } else
-        for (int s = 0; s < n_steps; ++s) {
-            const int st = s % kSt;
-            const int st1 = (s + 1) % kSt;
-            stress_delay(3, s);
-            issue_ts(Cfg::kTmemDV, Cfg::kTmemS, dDOm + st * kTile16, s > 0, p_full + kWG * kHv * (s & 1), (s >> 1) & 1,
-                     std::true_type{});  // dV += P^T dO
-            VTRACE(8 * s + 0);
-            if (s + 1 < n_steps) {
-                mbar_wait(q_full + st1, ((s + 1) / kSt) & 1);
-                tc_fence_after();
-                VTRACE(8 * s + 1);
-                issue_kk(Cfg::kTmemS, dK, dQk + st1 * kTile16);  // in-order after dV read P^T
-                mma_commit_e(s_full);
-            }
-            issue_ts(Cfg::kTmemDK, Cfg::kTmemDP, dQm + st * kTile16, s > 0, ds_full, s & 1, std::false_type{});  // dK += dS^T Q
-            VTRACE(8 * s + 2);
-            mma_commit_e(q_empty + st);
-            if (s + 1 < n_steps) {
-                issue_kk(Cfg::kTmemDP, dV, dDOk + st1 * kTile16);  // after dK read dS^T
-                mma_commit_e(dp_full);
-            }
+            mma_commit_e(dkv_full);
+            g0 += n_steps;
         }
-        mma_commit_e(dkv_full);
     } else if (warp >= 4) {
         // ------------------------------------------------------ P / dS warps
         regs_inc<Cfg::kRegsHi>();
         const int h = (warp - 4) >> 2;           // query-column group: [kQW h, kQW h + kQW)
         const int r = ((warp & 3) << 5) + lane;  // key row == TMEM lane
         const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
-        const int key = kb * 128 + r;
-        const bool key_ok = key < N;
         const float sc = p.scale_log2;
         constexpr int kCh = kQW / 32;            // 32-column chunks per warpgroup
+        uint32_t g0 = 0;  // steps of this CTA's earlier items
+        Item x_;
+        for (int it = 0; item_at(it, x_); ++it) {
+        const int bh = x_.bh, kb = x_.kb, i0 = x_.i0, n_steps = x_.n_steps;
+        const int key = kb * 128 + r;
+        const bool key_ok = key < N;
         uint64_t dbase = 0;
         if constexpr (kDrop) dbase = drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H);
         auto load_kmw = [&](int qi, uint32_t (&kw)[kCh]) {
@@ -761,19 +810,20 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             }
         };
         for (int s = 0; s < n_steps; ++s) {
-            const int st = s % kSt;
+            const uint32_t g = g0 + s;  // ring position (all items of this CTA)
+            const int st = g % kSt;
             const int i = i0 + s;
             const float* lse2 = sLD + st * 256 + kQW * h;
             const float* dsum = sLD + st * 256 + 128 + kQW * h;
-            const uint32_t sR = Cfg::kTmemS + (kDB ? (s & 1) * 128u : 0u);  // S / P^T region of this tile
+            const uint32_t sR = Cfg::kTmemS + (kDB ? (g & 1u) * 128u : 0u);  // S / P^T region of this tile
             // this key row's query bits (key-major copy, mha_dropmask_kernel).  (Loading them
             // one step ahead measured 11 % slower here -- registers -- unlike the forward.)
             uint32_t kmw[kCh];
 #pragma unroll
             for (int c = 0; c < kCh; ++c) kmw[c] = ~0u;
             if (kDrop && p.drop_mask_k) load_kmw(i, kmw);
-            mbar_wait(ld_full + st, (s / kSt) & 1);  // lse2 / D of this tile landed
-            mbar_wait(s_full + (kDB ? (s & 1) : 0), kDB ? ((s >> 1) & 1) : (s & 1));
+            mbar_wait(ld_full + st, (g / kSt) & 1);  // lse2 / D of this tile landed
+            mbar_wait(s_full + (kDB ? (g & 1u) : 0u), kDB ? ((g >> 1) & 1) : (g & 1));
             tc_fence_after();
             stress_delay(1, s);
             if ((warp == 4 || warp == 8) && lane == 0) VTRACE(1024 + 8 * s + 0 + (warp == 8 ? 4 : 0));
@@ -844,7 +894,7 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             auto publish = [&](int half) {  // this chunk's tcgen05.st has been waited on
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) arrive_mma(p_full + kWG * kHv * (s & 1) + kHv * h + half);
+                if (lane == 0) arrive_mma(p_full + kWG * kHv * (g & 1u) + kHv * h + half);
             };
             // P^T chunk by chunk: chunk 0 is stored (tcgen05.st) and published while chunk 1
             // is exponentiated.
@@ -878,7 +928,7 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             if ((warp == 4 || warp == 8) && lane == 0) VTRACE(1024 + 8 * s + 1 + (warp == 8 ? 4 : 0));
             stress_delay(2, s);
 
-            mbar_wait(dp_full, s & 1);
+            mbar_wait(dp_full, g & 1);
             tc_fence_after();
             if ((warp == 4 || warp == 8) && lane == 0) VTRACE(1024 + 8 * s + 2 + (warp == 8 ? 4 : 0));
             uint32_t dsp[kQW / 2];
@@ -963,7 +1013,7 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             }
         }
         // ---------------------------------------------------------- epilogue
-        mbar_wait(dkv_full, 0);
+        mbar_wait(dkv_full, it & 1);
         tc_fence_after();
         T16* dk = reinterpret_cast<T16*>(dk_out) + (static_cast<size_t>(bh) * N + key) * kD;
         T16* dv = reinterpret_cast<T16*>(dv_out) + (static_cast<size_t>(bh) * N + key) * kD;
@@ -1004,6 +1054,12 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                 }
             }
         }
+        // dV / dK are in registers: the next item's first dV / dK MMAs may overwrite them
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_free);
+        g0 += n_steps;
+        }  // items
     }
     if (!kPdlEarly) griddep_launch_dependents();
     tc_fence_before();
