@@ -437,7 +437,20 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     p.mask_words = (N + 127) / 128 * 4;
     p.status = status;
     if (kDrop && drop_mask) launch_dropmask(c, drop_mask, stream);
-    const dim3 grid = tile_grid((N + 255) / 256, BH, c->causal ? bh_group(BH, 2ll * N * kD * 2, true) : 1);  // K, V
+    const int nqb = (N + 255) / 256;
+    p.group = c->causal ? bh_group(BH, 2ll * N * kD * 2, true) : 1;  // K, V
+    p.items = nqb * BH;
+    // Persistent forward (one CTA per SM looping over the (unit, query block) items in
+    // the same order, static round robin) for short heads, N <= 1024 -- the same rule and
+    // reason as the dK/dV kernel; VATTN_FWD_PERSIST=0 / 1 forces either.
+    static const int fwd_persist_env = [] {
+        const char* e = getenv("VATTN_FWD_PERSIST");
+        return e ? atoi(e) : -1;
+    }();
+    const int sms = sm_count_cached();
+    const bool persist = (fwd_persist_env >= 0 ? fwd_persist_env == 1 : N <= 1024) && p.items > sms;
+    p.stride = persist ? sms : p.items;
+    const dim3 grid = persist ? dim3(static_cast<unsigned>(sms)) : tile_grid(nqb, BH, p.group);
     {
         ProfScope prof(stream, 0);
         launch_pdl(kern, grid, dim3(FwdCfg<kD>::kThreads), smem, stream, mq, mk, mv, mo, p);

@@ -52,6 +52,9 @@ struct FwdParams {
     // NaN / +inf score or an empty softmax sum (l == 0), the reference's domain_error
     // cases (online_softmax.cpp:33-34, 81-82); nullptr = unchecked
     unsigned int* status;
+    // items = (unit, 256-query block) in the order of the (nqb * G, units / G) grid
+    // (tile_grid); CTA c takes items c, c + stride, ... (persistent when stride < items)
+    int items, group, stride;
 };
 
 template <int kD>
@@ -76,7 +79,7 @@ struct FwdCfg {
     static constexpr int kHalves = VATTN_FWD_HALVES;
     static constexpr int kSmemX = kSmemKV + kStages * kTileBytes;  // [3 slots][2 tiles][kHalves][128] f32
     static constexpr int kSmemBar = kSmemX + 3 * 2 * kHalves * 128 * 4;
-    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 8 + 2 + 2;  // ..., o_done[2], s_free[2]
+    static constexpr int kNumBars = 1 + 2 * kStages + 2 + 8 + 2 + 2 + 3;  // ..., o_done[2], s_free[2], q_free, o_free[2]
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     // Warps: producer 0, MMA 1, TMEM allocator 2, idle 3, softmax warpgroups from warp 4.
     // setmaxnreg split of the CTA's launch allocation: 88 / 208 (384 threads x 168) or,
@@ -140,24 +143,38 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
     uint64_t* p_full = s_full + 2;
     uint64_t* o_done = p_full + 8;  // p_full: [tile][quarter]
     uint64_t* s_free = o_done + 2;  // kSepP: the softmax has S_t(j) in registers
+    // persistent CTAs: both tiles' O stores have left sQ (the next item's Q may land) /
+    // the epilogue has read O_t out of tensor memory (the next item's first P V may write)
+    uint64_t* q_free = s_free + 2;
+    uint64_t* o_free = q_free + 1;  // [2]
     constexpr bool kSepP = Cfg::kSepP;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
 
     const int warp = warp_id();
     const int lane = lane_id();
     const int nqb = (p.N + 255) / 256;
-    const int bh = grid_bh(nqb);
-    const int qblk = p.causal ? (nqb - 1 - grid_tile(nqb)) : grid_tile(nqb);
-    const int q0 = qblk * 256;
     const int N = p.N;
-
-    int nk[2];
+    const int lin = static_cast<int>(blockIdx.x + blockIdx.y * gridDim.x);
+    struct Item {
+        int bh, q0, nk[2], nkmax;
+    };
+    auto item_at = [&](int it, Item& x) -> bool {
+        const int L = lin + it * p.stride;
+        if (L >= p.items) return false;
+        const int W = nqb * p.group;  // grid x extent of tile_grid
+        const int bx = L % W, by = L / W;
+        x.bh = by * p.group + bx % p.group;
+        const int tile = bx / p.group;
+        const int qblk = p.causal ? (nqb - 1 - tile) : tile;
+        x.q0 = qblk * 256;
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        const int r0 = q0 + 128 * t;
-        nk[t] = r0 >= N ? 0 : (p.causal ? (r0 / 128 + 1) : p.n_kv);
-    }
-    const int nkmax = nk[0] > nk[1] ? nk[0] : nk[1];
+        for (int t = 0; t < 2; ++t) {
+            const int r0 = x.q0 + 128 * t;
+            x.nk[t] = r0 >= N ? 0 : (p.causal ? (r0 / 128 + 1) : p.n_kv);
+        }
+        x.nkmax = x.nk[0] > x.nk[1] ? x.nk[0] : x.nk[1];
+        return true;
+    };
 
     if (threadIdx.x == 0) {
         if ((smem_u32(smem) & 1023u) != 0) __trap();
@@ -171,7 +188,9 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
             for (int qq = 0; qq < 4; ++qq) mbar_init(p_full + 4 * t + qq, 4);  // one arrive per warp
             mbar_init(o_done + t, 1);
             mbar_init(s_free + t, 4 * Cfg::kHalves);  // one arrive per warp of the tile
+            mbar_init(o_free + t, 4 * Cfg::kHalves);
         }
+        mbar_init(q_free, 2);  // one arrive per tile (its O store thread)
         fence_barrier_init();
     }
     if (warp == Cfg::kAllocWarp) tmem_alloc<512>(tmem_slot);
@@ -191,28 +210,34 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
             tma_prefetch_desc(&tm_o);
-            const int nvalid = (nk[0] > 0) + (nk[1] > 0);
-            mbar_arrive_expect_tx(q_full, nvalid * Cfg::kTileBytes);
-            for (int t = 0; t < 2; ++t) {
-                if (nk[t] == 0) continue;
-                for (int b = 0; b < Cfg::kBoxes; ++b)
-                    tma_load_3d(sQ + t * Cfg::kTileBytes + b * 16384, &tm_q, q_full, b * 64,
-                                q0 + 128 * t, bh);
-            }
-            for (int j = 0; j < nkmax; ++j) {
-                stress_delay(4, j);
-#pragma unroll
-                for (int w = 0; w < 2; ++w) {
-                    const int pos = 2 * j + w;
-                    const int slot = pos % S;
-                    const uint32_t ph = (pos / S) & 1;
-                    mbar_wait<VATTN_SLEEP_PRODUCER>(kv_empty + slot, ph ^ 1);
-                    mbar_arrive_expect_tx(kv_full + slot, Cfg::kTileBytes);
-                    uint8_t* dst = sKV + slot * Cfg::kTileBytes;
-                    const CUtensorMap* map = w == 0 ? &tm_k : &tm_v;
+            uint32_t kvb = 0;  // K/V ring position at the item's start (2 per key step)
+            Item x;
+            for (int it = 0; item_at(it, x); ++it) {
+                const int bh = x.bh;
+                if (it > 0) mbar_wait(q_free, (it - 1) & 1);  // the previous item's O stores left sQ
+                const int nvalid = (x.nk[0] > 0) + (x.nk[1] > 0);
+                mbar_arrive_expect_tx(q_full, nvalid * Cfg::kTileBytes);
+                for (int t = 0; t < 2; ++t) {
+                    if (x.nk[t] == 0) continue;
                     for (int b = 0; b < Cfg::kBoxes; ++b)
-                        tma_load_3d(dst + b * 16384, map, kv_full + slot, b * 64, j * 128, bh);
+                        tma_load_3d(sQ + t * Cfg::kTileBytes + b * 16384, &tm_q, q_full, b * 64, x.q0 + 128 * t, bh);
                 }
+                for (int j = 0; j < x.nkmax; ++j) {
+                    stress_delay(4, j);
+#pragma unroll
+                    for (int w = 0; w < 2; ++w) {
+                        const uint32_t pos = kvb + 2 * j + w;
+                        const int slot = pos % S;
+                        const uint32_t ph = (pos / S) & 1;
+                        mbar_wait<VATTN_SLEEP_PRODUCER>(kv_empty + slot, ph ^ 1);
+                        mbar_arrive_expect_tx(kv_full + slot, Cfg::kTileBytes);
+                        uint8_t* dst = sKV + slot * Cfg::kTileBytes;
+                        const CUtensorMap* map = w == 0 ? &tm_k : &tm_v;
+                        for (int b = 0; b < Cfg::kBoxes; ++b)
+                            tma_load_3d(dst + b * 16384, map, kv_full + slot, b * 64, j * 128, bh);
+                    }
+                }
+                kvb += 2 * x.nkmax;
             }
         }
     } else if (warp == 1) {
@@ -224,22 +249,29 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
         const uint64_t dQ0 = umma_desc_sw128(smem_u32(sQ), 16, 1024);      // K-major Q tiles
         const uint64_t dK0 = umma_desc_sw128(smem_u32(sKV), 16, 1024);     // K-major K slots
         const uint64_t dV0 = umma_desc_sw128(smem_u32(sKV), 16384, 1024);  // MN-major V slots
+        uint32_t kvb = 0;              // K/V ring position at the item's start
+        uint32_t ts[2] = {0u, 0u};     // steps of tile t in this CTA's earlier items (phases)
         auto issue_s = [&](int t, int j) {
             const uint64_t qd = dQ0 + t * kTile16;
-            const uint64_t kd = dK0 + ((2 * j) % S) * kTile16;
+            const uint64_t kd = dK0 + ((kvb + 2 * j) % S) * kTile16;
 #pragma unroll
             for (int kk = 0; kk < kD / 16; ++kk)
                 mma_ss_e(tmem + 128 * t, desc_kmajor(qd, kk), desc_kmajor(kd, kk), idesc_s, kk > 0);
             mma_commit_e(s_full + t);
         };
+        int it = 0;  // item of this CTA (o_free phases)
         auto issue_pv = [&](int t, int j) {
-            const uint64_t vd = dV0 + ((2 * j + 1) % S) * kTile16;
+            const uint64_t vd = dV0 + ((kvb + 2 * j + 1) % S) * kTile16;
+            if (j == 0 && it > 0) {  // the previous item's epilogue has read O_t
+                mbar_wait_mma(o_free + t, (it - 1) & 1);
+                tc_fence_after();
+            }
             // P arrives in four 32-key quarters: each pair of K=16 steps starts as
             // soon as its quarter is in tensor memory (the softmax is still
             // exponentiating the rest of the row).
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
-                mbar_wait_mma(p_full + 4 * t + qq, j & 1);
+                mbar_wait_mma(p_full + 4 * t + qq, (ts[t] + j) & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int k2 = 0; k2 < 2; ++k2) {
@@ -251,67 +283,75 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
             }
             mma_commit_e(o_done + t);
         };
-        auto wait_kv = [&](int pos) {
+        auto wait_kv = [&](uint32_t pos) {
             mbar_wait_mma(kv_full + (pos % S), (pos / S) & 1);
             tc_fence_after();
         };
-        mbar_wait_mma(q_full, 0);
-        tc_fence_after();
-        VTRACE(3072);
-        if (nkmax > 0) {
-            wait_kv(0);
-            for (int t = 0; t < 2; ++t)
-                if (nk[t] > 0) issue_s(t, 0);
-            mma_commit_e(kv_empty + 0);
-        }
-        for (int j = 0; j < nkmax; ++j) {
-            stress_delay(3, j);
-            bool k_next = false;
-            if constexpr (kSepP) {
-                // S_t(j+1) as soon as the softmax read S_t(j); then P V of tile j
+        Item x;
+        for (; item_at(it, x); ++it) {
+            const int nk[2] = {x.nk[0], x.nk[1]};  // (registers: every use is unrolled over t)
+            const int nkmax = x.nkmax;
+            mbar_wait_mma(q_full, it & 1);
+            tc_fence_after();
+            VTRACE(3072);
+            if (nkmax > 0) {
+                wait_kv(kvb);
+                for (int t = 0; t < 2; ++t)
+                    if (nk[t] > 0) issue_s(t, 0);
+                mma_commit_e(kv_empty + kvb % S);
+            }
+            for (int j = 0; j < nkmax; ++j) {
+                stress_delay(3, j);
+                bool k_next = false;
+                if constexpr (kSepP) {
+                    // S_t(j+1) as soon as the softmax read S_t(j); then P V of tile j
 #pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    if (j + 1 < nk[t]) {
-                        if (!k_next) {
-                            wait_kv(2 * j + 2);
-                            k_next = true;
+                    for (int t = 0; t < 2; ++t) {
+                        if (j + 1 < nk[t]) {
+                            if (!k_next) {
+                                wait_kv(kvb + 2 * j + 2);
+                                k_next = true;
+                            }
+                            mbar_wait_mma(s_free + t, (ts[t] + j) & 1);
+                            tc_fence_after();
+                            VTRACE(8 * j + 4 * t + 1);
+                            issue_s(t, j + 1);
                         }
-                        mbar_wait_mma(s_free + t, j & 1);
-                        tc_fence_after();
-                        VTRACE(8 * j + 4 * t + 1);
-                        issue_s(t, j + 1);
                     }
+                    wait_kv(kvb + 2 * j + 1);
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        if (j < nk[t]) {
+                            issue_pv(t, j);
+                            VTRACE(8 * j + 4 * t + 0);
+                        }
+                    }
+                    mma_commit_e(kv_empty + (kvb + 2 * j + 1) % S);
+                    if (k_next) mma_commit_e(kv_empty + (kvb + 2 * j + 2) % S);
+                    continue;
                 }
-                wait_kv(2 * j + 1);
+                wait_kv(kvb + 2 * j + 1);
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
                     if (j < nk[t]) {
                         issue_pv(t, j);
                         VTRACE(8 * j + 4 * t + 0);
-                    }
-                }
-                mma_commit_e(kv_empty + (2 * j + 1) % S);
-                if (k_next) mma_commit_e(kv_empty + (2 * j + 2) % S);
-                continue;
-            }
-            wait_kv(2 * j + 1);
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                if (j < nk[t]) {
-                    issue_pv(t, j);
-                    VTRACE(8 * j + 4 * t + 0);
-                    if (j + 1 < nk[t]) {
-                        if (!k_next) {
-                            wait_kv(2 * j + 2);
-                            k_next = true;
+                        if (j + 1 < nk[t]) {
+                            if (!k_next) {
+                                wait_kv(kvb + 2 * j + 2);
+                                k_next = true;
+                            }
+                            VTRACE(8 * j + 4 * t + 1);
+                            issue_s(t, j + 1);
                         }
-                        VTRACE(8 * j + 4 * t + 1);
-                        issue_s(t, j + 1);
                     }
                 }
+                mma_commit_e(kv_empty + (kvb + 2 * j + 1) % S);
+                if (k_next) mma_commit_e(kv_empty + (kvb + 2 * j + 2) % S);
             }
-            mma_commit_e(kv_empty + (2 * j + 1) % S);
-            if (k_next) mma_commit_e(kv_empty + (2 * j + 2) % S);
+            kvb += 2 * nkmax;
+            ts[0] += nk[0];
+            ts[1] += nk[1];
         }
     } else if (warp >= Cfg::kMathWarp0) {
         // ----------------------------------------------------------- softmax
@@ -335,31 +375,36 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
         const uint32_t tP = (kSepP ? tmem + lane_base + Cfg::kTmemP + 64 * t : tmem + lane_base + 128 * t) + 16 * kQ * c;
         const uint32_t xbar = 3 + t;             // named barrier of the tile's warpgroups
         auto xslot = [&](int slot, int half) { return sX + ((slot * 2 + t) * kH + half) * 128; };
-        const int row = q0 + 128 * t + r;
         const float sc = p.scale_log2;
+        uint32_t ts = 0;  // steps of this tile in the CTA's earlier items (phases)
+        Item x_;
+        for (int it = 0; item_at(it, x_); ++it) {
+        const int bh = x_.bh, q0 = x_.q0;
+        const int row = q0 + 128 * t + r;
         DropRow drow{};
         if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H), row);
         float m_run = -INFINITY;  // running max, log2 units (already scaled)
         float l_run = 0.0f;       // this half's row sum
         bool bad = false;         // a NaN or +inf score in this row (FMNMX.NAN keeps NaN in mx)
-        const int ntile = t ? nk[1] : nk[0];
+        const int ntile = t ? x_.nk[1] : x_.nk[0];
         uint4 kw4_next = make_uint4(0u, 0u, 0u, 0u);
         if (kDrop && p.drop_mask && row < p.mask_words * 32 && ntile > 0)
             kw4_next = __ldg(reinterpret_cast<const uint4*>(p.drop_mask + (static_cast<size_t>(bh) * p.mask_words * 32 + row) *
                                                                               p.mask_words));
         for (int j = 0; j < ntile; ++j) {
-            mbar_wait<VATTN_SLEEP_MATH>(s_full + t, j & 1);
+            const uint32_t gj = ts + j;  // this tile's step across items (barrier phases)
+            mbar_wait<VATTN_SLEEP_MATH>(s_full + t, gj & 1);
             // O += P V of the previous tile has landed (issued before S(j), so this wait
             // returns at once): observing every o_done phase in order keeps the parity
             // waits unambiguous by construction (compute-sanitizer synccheck clean).
             // kSepP: S(j) is issued before P V(j-1), so that wait moves to just before O
             // or the P region is first touched in this step (o_wait below).
-            if (!kSepP && j > 0) mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (j - 1) & 1);
+            if (!kSepP && j > 0) mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (gj - 1) & 1);
             tc_fence_after();
             bool o_waited = !kSepP || j == 0;
             auto o_wait = [&] {
                 if (!o_waited) {
-                    mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (j - 1) & 1);
+                    mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (gj - 1) & 1);
                     tc_fence_after();
                     o_waited = true;
                 }
@@ -451,9 +496,9 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
             // row max: tree of 3-input maxima, then (two halves) the other half's through smem
             float mx = row_max<kC>(s);
             if constexpr (kH == 2) {
-                xslot(j & 1, c)[r] = mx;
+                xslot(gj & 1, c)[r] = mx;
                 named_bar_sync(xbar, 256);  // also: every S column of the tile is in registers
-                mx = fmax_nr(mx, xslot(j & 1, c ^ 1)[r]);
+                mx = fmax_nr(mx, xslot(gj & 1, c ^ 1)[r]);
             }
             bad |= !(mx < INFINITY);
             const float m_tile = mx * sc;
@@ -518,7 +563,7 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
         }
         if (ntile > 0) {
             // ------------------------------------------------------ epilogue
-            mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (ntile - 1) & 1);
+            mbar_wait<VATTN_SLEEP_MATH>(o_done + t, (ts + ntile - 1) & 1);
             tc_fence_after();
             float l_tot = l_run;
             if constexpr (kH == 2) {  // the row sum over both halves
@@ -558,6 +603,14 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
                 bulk_wait_read0();
             }
         }
+        // persistent hand-offs (also for a tile with no rows in this item): O_t has been
+        // read out of tensor memory, and this tile's O store has left sQ
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_free + t);
+        if (warp == Cfg::kMathWarp0 + 4 * kH * t && lane == 0) mbar_arrive(q_free);
+        ts += ntile;
+        }  // items
     }
     if (!kPdlEarly) griddep_launch_dependents();
     tc_fence_before();

@@ -384,7 +384,8 @@ for (B, H, N, d, causal, dtype, p) in [(2, 4, 1000, 128, True, torch.bfloat16, 0
                                        (4, 12, 900, 128, True, torch.float16, 0.0)]:
     q, k, v, do = workload(41 + N, (B, H, N, d), dtype)
     o, lse = vb.mha_forward(q, k, v, causal, dropout_p=p, seed=3)
-    out[(B, H, N, d, causal, p)] = [t.cpu() for t in vb.mha_backward(q, k, v, o, do, lse, causal, dropout_p=p, seed=3)]
+    g = vb.mha_backward(q, k, v, o, do, lse, causal, dropout_p=p, seed=3)
+    out[(B, H, N, d, causal, p)] = [t.cpu() for t in (*g, o, lse)]
 torch.save(out, os.environ["OUT"])
 print("OK")
 '''
@@ -405,14 +406,15 @@ def test_dq_workers_overlap_bitwise(tmp_path):
         assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
         res[w] = torch.load(path)
     for key, a in res["0"].items():
-        for name, x, y in zip(("dQ", "dK", "dV"), a, res["12"][key]):
+        for name, x, y in zip(("dQ", "dK", "dV", "O", "lse"), a, res["12"][key]):
             assert torch.equal(x, y), f"{key} {name}: overlapped dQ differs"
 
 
-def test_dkdv_persistent_bitwise(tmp_path):
-    """Persistent dK/dV CTAs (VATTN_DKDV_PERSIST=1: one CTA per SM looping over the
-    (unit, key tile) items, barrier phases carried across items) give the same bits as
-    one CTA per item, at d = 64 and 128, causal or not, ragged N and dropout."""
+@pytest.mark.parametrize("kernel", ["VATTN_DKDV_PERSIST", "VATTN_FWD_PERSIST"])
+def test_persistent_ctas_bitwise(tmp_path, kernel):
+    """Persistent dK/dV and forward CTAs (=1: one CTA per SM looping over the items,
+    barrier phases carried across items) give the same bits as one CTA per item, at
+    d = 64 and 128, causal or not, ragged N and dropout."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -420,12 +422,12 @@ def test_dkdv_persistent_bitwise(tmp_path):
     for mode in ("0", "1"):
         path = str(tmp_path / f"p{mode}.pt")
         r = subprocess.run([sys.executable, "-c", _WORKERS_CHILD], capture_output=True, text=True, timeout=600,
-                           env=dict(os.environ, VATTN_DKDV_PERSIST=mode, ROOT=root, OUT=path))
+                           env={**os.environ, kernel: mode, "ROOT": root, "OUT": path})
         assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
         res[mode] = torch.load(path)
     for key, a in res["0"].items():
-        for name, x, y in zip(("dQ", "dK", "dV"), a, res["1"][key]):
-            assert torch.equal(x, y), f"{key} {name}: persistent dK/dV differs"
+        for name, x, y in zip(("dQ", "dK", "dV", "O", "lse"), a, res["1"][key]):
+            assert torch.equal(x, y), f"{key} {name}: {kernel}=1 differs"
 
 
 # --------------------------------------- compute_dpsum and the mask digest --
