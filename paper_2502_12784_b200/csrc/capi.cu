@@ -422,10 +422,7 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     if (!make_map(&mq, q, BH, N, kD, kBF16) || !make_map(&mk, k, BH, N, kD, kBF16) ||
         !make_map(&mv, v, BH, N, kD, kBF16) || !make_map(&mo, o, BH, N, kD, kBF16))
         return fail(VATTN_ECUDA, g_err.empty() ? "cuTensorMapEncodeTiled failed" : g_err);
-    auto kern = mha_fwd_sm100_kernel<kD, kBF16, kDrop>;
     constexpr int smem = FwdCfg<kD>::kSmemBytes;
-    const cudaError_t attr_err = set_smem_once<mha_fwd_sm100_kernel<kD, kBF16, kDrop>>(smem);
-    if (attr_err != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(attr_err));
     FwdParams p;
     p.lse = lse;
     p.N = N;
@@ -453,7 +450,15 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
     const dim3 grid = persist ? dim3(static_cast<unsigned>(sms)) : tile_grid(nqb, BH, p.group);
     {
         ProfScope prof(stream, 0);
-        launch_pdl(kern, grid, dim3(FwdCfg<kD>::kThreads), smem, stream, mq, mk, mv, mo, p);
+        const cudaError_t attr_err = persist ? set_smem_once<mha_fwd_sm100_kernel<kD, kBF16, kDrop, true>>(smem)
+                                             : set_smem_once<mha_fwd_sm100_kernel<kD, kBF16, kDrop, false>>(smem);
+        if (attr_err != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(attr_err));
+        if (persist)
+            launch_pdl(mha_fwd_sm100_kernel<kD, kBF16, kDrop, true>, grid, dim3(FwdCfg<kD>::kThreads), smem, stream, mq, mk, mv,
+                       mo, p);
+        else
+            launch_pdl(mha_fwd_sm100_kernel<kD, kBF16, kDrop, false>, grid, dim3(FwdCfg<kD>::kThreads), smem, stream, mq, mk,
+                       mv, mo, p);
     }
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = g_launch_err;
@@ -659,15 +664,20 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
       }
     }
     if (!dkdv_launched) {
-        auto kern = mha_bwd_dkdv_kernel<kD, kBF16, kDrop>;
         // (the dQ workers' layout may be the larger one)
         constexpr int smem = DkdvCfg<kD>::kSmemBytes > DqGemmCfg<kD>::kSmemBytes ? DkdvCfg<kD>::kSmemBytes
                                                                                  : DqGemmCfg<kD>::kSmemBytes;
-        const cudaError_t ae = set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop>>(smem);
+        const bool multi = dkdv_ctas < p.dkdv_items;
+        const cudaError_t ae = multi ? set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop, false, true>>(smem)
+                                     : set_smem_once<mha_bwd_dkdv_kernel<kD, kBF16, kDrop, false, false>>(smem);
         if (ae != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(ae));
         ProfScope prof(stream, 1);
-        launch_pdl(kern, dim3(dkdv_ctas + W), dim3(DkdvCfg<kD>::kThreads), smem, stream, mq, mk, mv, mdo,
-                   L.materialize_ds ? mds : mq, mq, mdo, mdq, dk, dv, p);
+        if (multi)
+            launch_pdl(mha_bwd_dkdv_kernel<kD, kBF16, kDrop, false, true>, dim3(dkdv_ctas + W), dim3(DkdvCfg<kD>::kThreads),
+                       smem, stream, mq, mk, mv, mdo, L.materialize_ds ? mds : mq, mq, mdo, mdq, dk, dv, p);
+        else
+            launch_pdl(mha_bwd_dkdv_kernel<kD, kBF16, kDrop, false, false>, dim3(dkdv_ctas + W), dim3(DkdvCfg<kD>::kThreads),
+                       smem, stream, mq, mk, mv, mdo, L.materialize_ds ? mds : mq, mq, mdo, mdq, dk, dv, p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)
     // The dQ GEMM runs as the persistent worker kernel (one CTA per SM looping over the

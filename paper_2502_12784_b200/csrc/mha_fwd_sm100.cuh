@@ -119,7 +119,9 @@ constexpr bool kMaskedMufu = VATTN_FWD_MASKED_MUFU;
 #endif
 constexpr int kRescaleUnroll = VATTN_FWD_RESCALE_UNROLL;
 
-template <int kD, bool kBF16, bool kDrop>
+// kMulti: persistent CTAs looping over several items (host: N <= 1024); false compiles the
+// one-item-per-CTA kernel with the item loop folded away.
+template <int kD, bool kBF16, bool kDrop, bool kMulti = false>
 __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
     mha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
@@ -159,8 +161,9 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
         int bh, q0, nk[2], nkmax;
     };
     auto item_at = [&](int it, Item& x) -> bool {
-        const int L = lin + it * p.stride;
-        if (L >= p.items) return false;
+        if (!kMulti && it > 0) return false;
+        const int L = kMulti ? lin + it * p.stride : lin;
+        if (kMulti && L >= p.items) return false;
         const int W = nqb * p.group;  // grid x extent of tile_grid
         const int bx = L % W, by = L / W;
         x.bh = by * p.group + bx % p.group;
