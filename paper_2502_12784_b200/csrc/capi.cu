@@ -409,9 +409,8 @@ void launch_dropmask(const vattn_config* c, uint32_t* mask, cudaStream_t stream)
     const int nt = (c->seq_len + 127) / 128;
     const unsigned pairs = c->causal ? static_cast<unsigned>(nt) * (nt + 1) / 2 : static_cast<unsigned>(nt) * nt;
     ProfScope prof(stream, 4);
-    const HashMul hm{4u, 32u, 1u, 2u};  // run-time multipliers (sm100_ptx.cuh, drop_keep_word_fma)
     launch_pdl(mha_dropmask_kernel, dim3(pairs, static_cast<unsigned>(units(c))), dim3(256), 0, stream, mask, nt * 128,
-               H, bh_off, seed, thresh, c->causal, hm);
+               H, bh_off, seed, thresh, c->causal);
 }
 
 template <int kD, bool kBF16, bool kDrop>

@@ -146,7 +146,7 @@ struct BwdParams {
 // the key-major words, staged in shared memory so both copies leave as 16-byte stores.  Causal: tile pairs above the diagonal are skipped (masked positions; no
 // kernel reads their bits).
 __global__ void __launch_bounds__(256) mha_dropmask_kernel(uint32_t* __restrict__ mask, int Npad, int H, int bh_off,
-                                                           uint64_t seed, uint64_t thresh, int causal, HashMul hm) {
+                                                           uint64_t seed, uint64_t thresh, int causal) {
     griddep_start();
     __shared__ uint32_t qm[128][5];  // [query][key word] (+1 pad)
     __shared__ uint32_t km[128][5];  // [key][query word]
@@ -175,7 +175,6 @@ __global__ void __launch_bounds__(256) mha_dropmask_kernel(uint32_t* __restrict_
         bool tie, wrap;
         uint32_t w = th.hi < 0x80000000u ? drop_keep_word<true>(dr, col0, th.hi, tie, wrap)
                                          : drop_keep_word<false>(dr, col0, th.hi, tie, wrap);
-        (void)hm;
         if (tie || wrap) {  // a high word tied (p ~ 2^-32 per position) or K's low word wraps: exact
             w = 0;
 #pragma unroll 1

@@ -908,39 +908,6 @@ VATTN_DEV DropThresh drop_thresh_split(uint64_t thresh) {
     const uint64_t t11 = thresh << 11;
     return {thresh, static_cast<uint32_t>(t11 >> 32), static_cast<uint32_t>(t11)};
 }
-// The mask kernel's form: the integer ALU pipe bounds it (ncu: 89 % busy, FMA pipe
-// 18 %), so part of the 64-bit shifts run as multiplies on the FMA pipe -- x >> k as
-// mul.hi(x, 2^(32-k)), x << k as x * 2^k -- with the multipliers passed at run time so
-// ptxas cannot strength-reduce them back to SHF.  Sets `tie` when the high words tie
-// (the caller redoes those positions exactly); otherwise returns the keep bit.
-struct HashMul {
-    uint32_t m4, m32;  // 4 (>> 30, << 2), 32 (>> 27, << 5)
-    uint32_t one;      // 1: a * one + c64 as IMAD.WIDE (64-bit add with the carry in the high word)
-    uint32_t m2;       // 2 (>> 31)
-};
-VATTN_DEV bool drop_keep_mul(const DropRow& r, uint32_t col, uint32_t th_hi, const HashMul& m, bool& tie) {
-    const uint64_t c = (r.s ^ (static_cast<uint64_t>(col) + r.k)) + 0x9e3779b97f4a7c15ull;
-    uint32_t xl = static_cast<uint32_t>(c), xh = static_cast<uint32_t>(c >> 32);
-    {  // x ^= x >> 30
-        const uint32_t a = xh >> 30, b = xh * m.m4 + __umulhi(xl, m.m4);
-        xh ^= a;
-        xl ^= b;
-    }
-    {  // x *= 0xbf58476d1ce4e5b9
-        const uint64_t pr = static_cast<uint64_t>(xl) * 0x1ce4e5b9u;
-        xh = static_cast<uint32_t>(pr >> 32) + xl * 0xbf58476du + xh * 0x1ce4e5b9u;
-        xl = static_cast<uint32_t>(pr);
-    }
-    {  // x ^= x >> 27
-        const uint32_t a = __umulhi(xh, m.m32), b = xh * m.m32 + __umulhi(xl, m.m32);
-        xh ^= a;
-        xl ^= b;
-    }
-    uint32_t zh = __umulhi(xl, 0x133111ebu) + xl * 0x94d049bbu + xh * 0x133111ebu;  // high word of x * C2
-    zh ^= zh >> 31;
-    tie = zh == th_hi;
-    return zh > th_hi;
-}
 // 32 consecutive keys col0 .. col0 + 31 of one row at once (the mask kernel's word),
 // returning the keep bits (bit b = key col0 + b) and setting `tie` when any high word
 // tied (the caller then redoes the word exactly).  Per word, K = k + col0 keeps its high
@@ -1001,16 +968,6 @@ VATTN_DEV uint32_t warp_transpose32(uint32_t x, int lane) {
     return x;
 }
 
-VATTN_DEV bool drop_keep_fast(const DropRow& r, int col, const DropThresh& th) {
-    uint64_t x = (r.s ^ (static_cast<uint64_t>(col) + r.k)) + 0x9e3779b97f4a7c15ull;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-    x ^= x >> 27;
-    const uint32_t lo = static_cast<uint32_t>(x), hi = static_cast<uint32_t>(x >> 32);
-    uint32_t zh = __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;  // high word of x * C2
-    zh ^= zh >> 31;                                                                    // high word of z
-    if (zh != th.hi) return zh > th.hi;
-    return drop_keep(r, col, th.t);  // tie
-}
 // Round to the 16-bit storage type and back (the reference narrows P once
 // before dropout and once after the 1/(1-p) scaling, attention_forward.cpp:94-106).
 template <bool kBF16>
