@@ -539,8 +539,19 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
         } else {
             if (!kMulti && it > 0) return false;
             const int L = kMulti ? cta + it * G : cta;
-            if (kMulti && L >= p.dkdv_items) return false;
-            grid_item_tail_n(L, p.dkdv_items, p.n_q, p.tail_units, x.bh, x.kb);
+            if (kMulti && !p.causal && L >= p.dkdv_items) return false;
+            if (kMulti && p.causal) {
+                // causal items differ n_q-fold in length: hand them out longest first (key
+                // tile-major) in a zigzag over the CTAs, so every CTA's total is balanced
+                // (short heads only: a key tile of every unit fits in L2 at once)
+                const int units_ = p.dkdv_items / p.n_q;
+                const int idx = (it & 1) ? it * G + (G - 1 - cta) : L;
+                if (idx >= p.dkdv_items) return false;
+                x.kb = idx / units_;
+                x.bh = idx - x.kb * units_;
+            } else {
+                grid_item_tail_n(L, p.dkdv_items, p.n_q, p.tail_units, x.bh, x.kb);
+            }
         }
         // causal: both CTAs of a pair start at the lower key tile's diagonal (the upper
         // tile's first query tile is fully masked)

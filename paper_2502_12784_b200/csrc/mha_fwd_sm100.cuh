@@ -163,11 +163,22 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
     auto item_at = [&](int it, Item& x) -> bool {
         if (!kMulti && it > 0) return false;
         const int L = kMulti ? lin + it * p.stride : lin;
-        if (kMulti && L >= p.items) return false;
-        const int W = nqb * p.group;  // grid x extent of tile_grid
-        const int bx = L % W, by = L / W;
-        x.bh = by * p.group + bx % p.group;
-        const int tile = bx / p.group;
+        if (kMulti && !p.causal && L >= p.items) return false;
+        int tile;
+        if (kMulti && p.causal) {
+            // causal items differ in length: longest first (tile-major) in a zigzag over
+            // the CTAs so every CTA's total is balanced (short heads: their K/V fit in L2)
+            const int units_ = p.items / nqb;
+            const int idx = (it & 1) ? it * p.stride + (p.stride - 1 - lin) : L;
+            if (idx >= p.items) return false;
+            tile = idx / units_;
+            x.bh = idx - tile * units_;
+        } else {
+            const int W = nqb * p.group;  // grid x extent of tile_grid
+            const int bx = L % W, by = L / W;
+            x.bh = by * p.group + bx % p.group;
+            tile = bx / p.group;
+        }
         const int qblk = p.causal ? (nqb - 1 - tile) : tile;
         x.q0 = qblk * 256;
 #pragma unroll
