@@ -168,13 +168,14 @@ __global__ void __launch_bounds__(256) mha_dropmask_kernel(uint32_t* __restrict_
     griddep_wait();
     const DropRow dr = drop_row(drop_bh_base(seed, (bh + bh_off) / H, (bh + bh_off) % H), i * 128 + qs * 32 + lane);
     const DropThresh th = drop_thresh_split(thresh);
+    const uint32_t one = blockDim.x / 256u;  // always 256 threads: 1, opaque to the compiler (drop_keep_word)
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
         const int kw = kh * 2 + c;  // key word within the tile
         const uint32_t col0 = static_cast<uint32_t>(j * 128 + kw * 32);
         bool tie, wrap;
-        uint32_t w = th.hi < 0x80000000u ? drop_keep_word<true>(dr, col0, th.hi, tie, wrap)
-                                         : drop_keep_word<false>(dr, col0, th.hi, tie, wrap);
+        uint32_t w = th.hi < 0x80000000u ? drop_keep_word<true>(dr, col0, th.hi, one, tie, wrap)
+                                         : drop_keep_word<false>(dr, col0, th.hi, one, tie, wrap);
         if (tie || wrap) {  // a high word tied (p ~ 2^-32 per position) or K's low word wraps: exact
             w = 0;
 #pragma unroll 1

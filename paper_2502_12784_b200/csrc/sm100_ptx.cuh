@@ -919,8 +919,21 @@ VATTN_DEV DropThresh drop_thresh_split(uint64_t thresh) {
 // second xor-shift and the high word of x2 * C2 -- the same integers as drop_keep.
 // kLowThresh (th_hi < 2^31, i.e. p < 1/2): the final z ^= z >> 31 only flips bit 0 of
 // high words >= 2^31, which are above th_hi either way, so it is skipped.
+//
+// Issue balance (the mask kernel is bound by instruction issue, shared between the integer
+// ALU pipe and the FMA pipe that runs IMAD): the low-word add's carry-out feeds the high
+// word directly (add.cc / addc), hi(x1 * C1lo)'s per-word share is linear in that high
+// word (one IMAD), the keys are walked downwards so each keep bit shifts in through a
+// carry (w = 2 w + (zh > th_hi), two adds, no per-bit constant), the tie flag is a
+// predicate AND, and the key index decrement and the >> 27 of the high word run as
+// IMAD / IMAD.HI by `one` (a value the compiler cannot fold: the caller passes
+// blockDim.x / 256 = 1).  ~21 SASS instructions per key against ~27 for the plain form
+// (VATTN_DROPKEEP=0, kept for A/B runs).
+#ifndef VATTN_DROPKEEP
+#define VATTN_DROPKEEP 1
+#endif
 template <bool kLowThresh>
-VATTN_DEV uint32_t drop_keep_word(const DropRow& r, uint32_t col0, uint32_t th_hi, bool& tie, bool& wrap) {
+VATTN_DEV uint32_t drop_keep_word(const DropRow& r, uint32_t col0, uint32_t th_hi, uint32_t one, bool& tie, bool& wrap) {
     constexpr uint32_t kGlo = 0x7f4a7c15u, kGhi = 0x9e3779b9u;
     constexpr uint32_t kC1lo = 0x1ce4e5b9u, kC1hi = 0xbf58476du;
     constexpr uint32_t kC2lo = 0x133111ebu, kC2hi = 0x94d049bbu;
@@ -932,6 +945,8 @@ VATTN_DEV uint32_t drop_keep_word(const DropRow& r, uint32_t col0, uint32_t th_h
     const uint32_t h0a = xh + kGhi, h0b = h0a + 1u;              // high word of x0 (carry 0 / 1)
     const uint32_t h1a = h0a ^ (h0a >> 30), h1b = h0b ^ (h0b >> 30);  // high word of x1
     const uint32_t hca = h1a * kC1lo, hcb = h1b * kC1lo;          // its share of hi(x1 * C1)
+#if VATTN_DROPKEEP == 0
+    (void)one;
     uint32_t w = 0;
     bool t = false;
 #pragma unroll 8
@@ -953,6 +968,34 @@ VATTN_DEV uint32_t drop_keep_word(const DropRow& r, uint32_t col0, uint32_t th_h
     }
     tie = t;
     return w;
+#else
+    uint32_t hcd = hcb - hca, k2 = hca - h0a * hcd;                // hc = hi0 * hcd + k2
+    asm("mov.b32 %0, %0;" : "+r"(hcd));                            // keep the compiler from
+    asm("mov.b32 %0, %0;" : "+r"(k2));                             // re-expanding hc
+    const uint32_t k32 = one << 5, nth = ~th_hi;                   // umulhi(x, 32) = x >> 27
+    uint32_t w = 0, kb = Klo + 32u;
+    bool nt = true;
+#pragma unroll 8
+    for (int b = 31; b >= 0; --b) {
+        asm("mad.lo.u32 %0, %1, -1, %0;" : "+r"(kb) : "r"(one));  // Klo + b
+        const uint32_t xl = kb ^ slo;
+        uint32_t lo0, hi0;                                         // x0 = x + G
+        asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;" : "=r"(lo0), "=r"(hi0) : "r"(xl), "n"(kGlo), "r"(h0a));
+        const uint32_t lo1 = lo0 ^ __funnelshift_r(lo0, hi0, 30);  // x ^= x >> 30 (low word)
+        const uint64_t pr = static_cast<uint64_t>(lo1) * kC1lo;
+        const uint32_t lo2 = static_cast<uint32_t>(pr);
+        const uint32_t hi2 = static_cast<uint32_t>(pr >> 32) + lo1 * kC1hi + (hi0 * hcd + k2);
+        const uint32_t lo3 = lo2 ^ __funnelshift_r(lo2, hi2, 27);  // x ^= x >> 27
+        const uint32_t hi3 = hi2 ^ __umulhi(hi2, k32);
+        uint32_t zh = __umulhi(lo3, kC2lo) + lo3 * kC2hi + hi3 * kC2lo;  // high word of x * C2
+        if constexpr (!kLowThresh) zh ^= zh >> 31;
+        nt &= zh != th_hi;
+        uint32_t sink;                                             // carry of zh + ~th_hi = (zh > th_hi)
+        asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %1, %1;" : "=r"(sink), "+r"(w) : "r"(zh), "r"(nth));
+    }
+    tie = !nt;
+    return w;
+#endif
 }
 
 // 32 x 32 bit transpose across a warp: lane l holds row l (bit c = column c) in, column l
