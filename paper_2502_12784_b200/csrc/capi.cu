@@ -444,20 +444,29 @@ int launch_forward(const vattn_config* c, const void* q, const void* k, const vo
         return e ? atoi(e) : -1;
     }();
     const int sms = sm_count_cached();
-    const bool persist = (fwd_persist_env >= 0 ? fwd_persist_env == 1 : N <= 1024) && p.items > sms;
+    // (the in-softmax hash variant, dropout without a mask buffer, is one-item-per-CTA only)
+    const bool persist = (fwd_persist_env >= 0 ? fwd_persist_env == 1 : N <= 1024) && p.items > sms && !(kDrop && !drop_mask);
     p.stride = persist ? sms : p.items;
     const dim3 grid = persist ? dim3(static_cast<unsigned>(sms)) : tile_grid(nqb, BH, p.group);
     {
         ProfScope prof(stream, 0);
-        const cudaError_t attr_err = persist ? set_smem_once<mha_fwd_sm100_kernel<kD, kBF16, kDrop, true>>(smem)
-                                             : set_smem_once<mha_fwd_sm100_kernel<kD, kBF16, kDrop, false>>(smem);
-        if (attr_err != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(attr_err));
-        if (persist)
-            launch_pdl(mha_fwd_sm100_kernel<kD, kBF16, kDrop, true>, grid, dim3(FwdCfg<kD>::kThreads), smem, stream, mq, mk, mv,
+        constexpr int kMode = kDrop ? 1 : 0;  // dropout with a mask buffer / none
+        if (kDrop && !drop_mask) {
+            const cudaError_t attr_err = set_smem_once<mha_fwd_sm100_kernel<kD, kBF16, 2, false>>(smem);
+            if (attr_err != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(attr_err));
+            launch_pdl(mha_fwd_sm100_kernel<kD, kBF16, 2, false>, grid, dim3(FwdCfg<kD>::kThreads), smem, stream, mq, mk, mv,
                        mo, p);
-        else
-            launch_pdl(mha_fwd_sm100_kernel<kD, kBF16, kDrop, false>, grid, dim3(FwdCfg<kD>::kThreads), smem, stream, mq, mk,
-                       mv, mo, p);
+        } else {
+            const cudaError_t attr_err = persist ? set_smem_once<mha_fwd_sm100_kernel<kD, kBF16, kMode, true>>(smem)
+                                                 : set_smem_once<mha_fwd_sm100_kernel<kD, kBF16, kMode, false>>(smem);
+            if (attr_err != cudaSuccess) return fail(VATTN_ECUDA, cudaGetErrorString(attr_err));
+            if (persist)
+                launch_pdl(mha_fwd_sm100_kernel<kD, kBF16, kMode, true>, grid, dim3(FwdCfg<kD>::kThreads), smem, stream, mq, mk,
+                           mv, mo, p);
+            else
+                launch_pdl(mha_fwd_sm100_kernel<kD, kBF16, kMode, false>, grid, dim3(FwdCfg<kD>::kThreads), smem, stream, mq, mk,
+                           mv, mo, p);
+        }
     }
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = g_launch_err;

@@ -80,7 +80,11 @@ struct FwdCfg {
     static constexpr int kSmemX = kSmemKV + kStages * kTileBytes;  // [3 slots][2 tiles][kHalves][128] f32
     static constexpr int kSmemBar = kSmemX + 3 * 2 * kHalves * 128 * 4;
     static constexpr int kNumBars = 1 + 2 * kStages + 2 + 8 + 2 + 2 + 3;  // ..., o_done[2], s_free[2], q_free, o_free[2]
-    static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
+    // dropout keep bits, staged per softmax thread one key tile ahead (cp.async):
+    // [2 buffers][256 kHalves threads][16 B] -- in registers the prefetch spilled S
+    static constexpr int kSmemMask = (kSmemBar + kNumBars * 8 + 16 + 127) / 128 * 128;
+    static constexpr int kMaskBuf = 256 * kHalves * 16;
+    static constexpr int kSmemBytes = kSmemMask + 2 * kMaskBuf;
     // Warps: producer 0, MMA 1, TMEM allocator 2, idle 3, softmax warpgroups from warp 4.
     // setmaxnreg split of the CTA's launch allocation: 88 / 208 (384 threads x 168) or,
     // two halves (640 threads x 96), VATTN_FWD_REGS_LO / VATTN_FWD_REGS_HI.
@@ -121,7 +125,11 @@ constexpr int kRescaleUnroll = VATTN_FWD_RESCALE_UNROLL;
 
 // kMulti: persistent CTAs looping over several items (host: N <= 1024); false compiles the
 // one-item-per-CTA kernel with the item loop folded away.
-template <int kD, bool kBF16, bool kDrop, bool kMulti = false>
+// kDropMode: 0 no dropout; 1 keep bits read from the pre-hashed mask (mha_dropmask_kernel);
+// 2 keep bits hashed in the softmax (no mask buffer).  Separate instantiations: the
+// in-softmax hash loop needs registers that, compiled into the mask path, made ptxas spill
+// S columns to local memory on every tile.
+template <int kD, bool kBF16, int kDropMode, bool kMulti = false>
 __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
     mha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
@@ -129,6 +137,8 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
                          const __grid_constant__ CUtensorMap tm_o, const FwdParams p) {
     VCTA(0, 0);
     griddep_start();
+    constexpr bool kDrop = kDropMode != 0;
+    constexpr bool kMaskBits = kDropMode == 1;
     using Cfg = FwdCfg<kD>;
     constexpr int kVtraceKid = 0;
     (void)kVtraceKid;
@@ -395,16 +405,21 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
         for (int it = 0; item_at(it, x_); ++it) {
         const int bh = x_.bh, q0 = x_.q0;
         const int row = q0 + 128 * t + r;
-        DropRow drow{};
-        if constexpr (kDrop) drow = drop_row(drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H), row);
         float m_run = -INFINITY;  // running max, log2 units (already scaled)
         float l_run = 0.0f;       // this half's row sum
         bool bad = false;         // a NaN or +inf score in this row (FMNMX.NAN keeps NaN in mx)
         const int ntile = t ? x_.nk[1] : x_.nk[0];
-        uint4 kw4_next = make_uint4(0u, 0u, 0u, 0u);
-        if (kDrop && p.drop_mask && row < p.mask_words * 32 && ntile > 0)
-            kw4_next = __ldg(reinterpret_cast<const uint4*>(p.drop_mask + (static_cast<size_t>(bh) * p.mask_words * 32 + row) *
-                                                                              p.mask_words));
+        // this row's keep bits of key tile jt -> staging buffer buf (cp.async, one tile ahead;
+        // rows past the mask (padding) read zeros)
+        const uint32_t mslot = smem_u32(smem + Cfg::kSmemMask) + static_cast<uint32_t>(g * 128 + r) * 16u;
+        auto mask_fetch = [&](int jt, uint32_t buf) {
+            const bool ok = row < p.mask_words * 32;
+            const uint32_t* src =
+                ok ? p.drop_mask + (static_cast<size_t>(bh) * p.mask_words * 32 + row) * p.mask_words + jt * 4 : p.drop_mask;
+            cp_async16(mslot + buf * Cfg::kMaskBuf, src, ok ? 16u : 0u);
+            cp_async_commit();
+        };
+        if (kMaskBits && ntile > 0) mask_fetch(0, ts & 1);
         for (int j = 0; j < ntile; ++j) {
             const uint32_t gj = ts + j;  // this tile's step across items (barrier phases)
             mbar_wait<VATTN_SLEEP_MATH>(s_full + t, gj & 1);
@@ -425,12 +440,12 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
             };
             stress_delay(1, j);
             if ((warp & 3) == 0 && lane == 0 && c == 0) VTRACE(1024 + 8 * j + 4 * t + 0);
-            // this row's keep bits of key tile j, loaded one step ahead (the mask streams
-            // from HBM: its latency stays off the softmax)
-            const uint4 kw4 = kw4_next;
-            if (kDrop && p.drop_mask && row < p.mask_words * 32 && j + 1 < ntile)
-                kw4_next = __ldg(reinterpret_cast<const uint4*>(p.drop_mask + (static_cast<size_t>(bh) * p.mask_words * 32 + row) *
-                                                                                  p.mask_words + (j + 1) * 4));
+            // this row's keep bits of key tile j landed during the previous step; fetch j + 1
+            // (the mask streams from HBM: its latency stays off the softmax)
+            if constexpr (kMaskBits) {
+                cp_async_wait_all();
+                if (j + 1 < ntile) mask_fetch(j + 1, (gj + 1) & 1);
+            }
             float s[kC];
 #pragma unroll
             for (int x = 0; x < kC / 32; ++x) tmem_ld32f(tS + 32 * x, s + 32 * x);
@@ -457,13 +472,21 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
                 const int qq = kQ * c + qi;  // quarter of the tile row
                 const float2 sc2 = make_float2(sc, sc);
                 const float2 nm2 = make_float2(-mu, -mu);
-                uint32_t kw = qq == 0 ? kw4.x : qq == 1 ? kw4.y : qq == 2 ? kw4.z : kw4.w;
-                if (kDrop && !p.drop_mask) {  // no pre-hashed bits: hash this quarter's 32 keys here
+                uint32_t kw = 0;
+                if constexpr (kMaskBits) kw = lds_u32(mslot + (gj & 1) * Cfg::kMaskBuf + 4u * qq);
+                if constexpr (kDropMode == 2) {  // no pre-hashed bits: hash this quarter's 32 keys here
+                    // (the row's hash prefix is rebuilt per quarter rather than held in four
+                    // registers across the tile loop)
+                    const DropRow drow = drop_row(drop_bh_base(p.drop_seed, (bh + p.bh_off) / p.H, (bh + p.bh_off) % p.H), row);
                     kw = 0;
 #pragma unroll 1
                     for (int b = 0; b < 32; ++b)
                         kw |= static_cast<uint32_t>(drop_keep(drow, j * 128 + 32 * qq + b, p.drop_thresh)) << b;
                 }
+                uint32_t ks[8];
+#pragma unroll
+                for (int sh = 0; sh < 8; ++sh) ks[sh] = kw << sh;
+                const float2 inv2 = make_float2(p.inv_keep, p.inv_keep);
 #pragma unroll
                 for (int x = 0; x < 16; ++x) {
                     const int e = 32 * qi + 2 * x;
@@ -479,10 +502,9 @@ __global__ void __launch_bounds__(FwdCfg<kD>::kThreads, 1)
                     pk[x] = pack2<kBF16>(pp.x, pp.y);
                     if constexpr (kDrop) {
                         // dropout on the 16-bit P: f16(f16(P) * 1/(1-p)) or 0
-                        // (attention_forward.cpp:94-106)
-                        const float2 f = unpack2<kBF16>(pk[x]);
-                        const bool k0 = (kw >> (2 * x)) & 1u, k1 = (kw >> (2 * x + 1)) & 1u;
-                        pk[x] = pack2<kBF16>(k0 ? f.x * p.inv_keep : 0.0f, k1 ? f.y * p.inv_keep : 0.0f);
+                        // (attention_forward.cpp:94-106); dropped lanes masked to +0
+                        const float2 f = fmul2(unpack2<kBF16>(pk[x]), inv2);
+                        pk[x] = pack2<kBF16>(f.x, f.y) & keep_mask16(ks, x);
                     }
                 }
                 (void)kw;

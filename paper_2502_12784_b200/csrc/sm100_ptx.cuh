@@ -835,6 +835,32 @@ VATTN_DEV float2 fmul2(float2 a, float2 b) {
     return d;
 }
 
+// Per-thread 16-byte global -> shared copy (LDGSTS, L2 only); bytes = 0 zero-fills.
+VATTN_DEV void cp_async16(uint32_t dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+VATTN_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+VATTN_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+VATTN_DEV uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+VATTN_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+// Keep mask of packed pair x (keys 2x, 2x + 1) of a 32-key word kw, as two 16-bit lanes
+// of all ones (kept) or zeros, from the word's shifts ks[s] = kw << s: key k sits in the
+// sign bit of byte k / 8 of ks[7 - k % 8], and PRMT's sign-replicate selectors spread it
+// over the lane -- one PRMT per pair, the eight shifts shared by the word's 16 pairs.
+VATTN_DEV uint32_t keep_mask16(const uint32_t (&ks)[8], int x) {
+    const int m = x >> 2, s0 = 7 - 2 * (x & 3);
+    const uint32_t sel = static_cast<uint32_t>((8 | m) | ((8 | m) << 4) | ((12 | m) << 8) | ((12 | m) << 12));
+    return prmt(ks[s0], ks[s0 - 1], sel);
+}
+
 // Two ex2_poly on packed fp32 pairs (FFMA2 / FADD2): ~5.5 issue slots per element.
 VATTN_DEV float2 ex2_poly2(float2 x) {
     x.x = fmaxf(x.x, -127.0f);
