@@ -896,11 +896,15 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
             auto pack_chunk = [&](uint32_t (&pk)[16], int x0) {
                 if constexpr (kDrop) {  // dV operand f16(P * drop) (attention_backward.cpp:163-167)
                     const float2 ik2 = make_float2(p.inv_keep, p.inv_keep);
+                    uint32_t ks[8];  // this chunk's keep word, shifted: PRMT lane masks (keep_mask16)
+                    const uint32_t kw = static_cast<uint32_t>(keepm >> x0);
+#pragma unroll
+                    for (int sh = 0; sh < 8; ++sh) ks[sh] = kw << sh;
 #pragma unroll
                     for (int x = 0; x < 16; ++x) {
                         const int e = x0 + 2 * x;
                         const float2 pd = fmul2(make_float2(pr[e], pr[e + 1]), ik2);  // packed FMUL2
-                        pk[x] = pack2<kBF16>((keepm >> e) & 1 ? pd.x : 0.0f, (keepm >> (e + 1)) & 1 ? pd.y : 0.0f);
+                        pk[x] = pack2<kBF16>(pd.x, pd.y) & keep_mask16(ks, x);      // dropped lanes +0
                     }
                 } else {
 #pragma unroll

@@ -860,6 +860,12 @@ VATTN_DEV uint32_t keep_mask16(const uint32_t (&ks)[8], int x) {
     const uint32_t sel = static_cast<uint32_t>((8 | m) | ((8 | m) << 4) | ((12 | m) << 8) | ((12 | m) << 12));
     return prmt(ks[s0], ks[s0 - 1], sel);
 }
+// The same for one key k of the word as a 32-bit lane (all ones = kept): the sign of byte
+// k / 8 of ks[7 - k % 8] replicated over the four bytes.
+VATTN_DEV uint32_t keep_mask32(const uint32_t (&ks)[8], int k) {
+    const uint32_t n = static_cast<uint32_t>(8 | (k >> 3));
+    return prmt(ks[7 - (k & 7)], 0u, n * 0x1111u);
+}
 
 // Two ex2_poly on packed fp32 pairs (FFMA2 / FADD2): ~5.5 issue slots per element.
 VATTN_DEV float2 ex2_poly2(float2 x) {
