@@ -10,6 +10,10 @@ mkdir -p "$OUT"
 CFG_D64='[[2,4,2048,64,1,"fp16",0.0],[4,8,1024,64,0,"bf16",0.0]]'
 for lib in tools/variants/stress_legacy.so paper_2502_12784_b200/libvattn_b200_stress.so; do
   name=$(basename $lib .so)
+  if [ ! -f "$lib" ]; then  # a missing build must not read as a trapped run
+    echo "$name: MISSING ($lib) -- build it first (tools/build_stress_legacy.sh / make)"
+    continue
+  fi
   fails=0
   for i in $(seq 1 $RUNS); do
     VATTN_LIB=$lib timeout 300 python tests/stress_child.py "$CFG_D64" 8 > "$OUT/${name}_$i.log" 2>&1
