@@ -184,13 +184,14 @@ bool make_map(CUtensorMap* m, const void* ptr, int BH, int N, int D, bool bf16, 
     return true;
 }
 
-// dS^T scratch viewed as [tiles][128 keys][128 queries] 16-bit, 64-query x 128-key boxes.
-bool encode_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16) {
+// dS^T scratch viewed as [tiles][128 keys][128 queries] 16-bit, 64-query x `rows`-key
+// boxes (128: the dQ GEMM's loads; 32: the dK/dV kernel's per-warp stores).
+bool encode_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16, int rows = 128) {
     EncodeFn enc = encode_fn();
     if (!enc || tiles > (1ll << 31) - 1) return false;
     const cuuint64_t dims[3] = {128, 128, static_cast<cuuint64_t>(tiles)};
     const cuuint64_t strides[2] = {256, 32768};
-    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(rows), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     auto encode = [&] {
         return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
@@ -205,14 +206,14 @@ bool encode_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16) 
     return r == CUDA_SUCCESS;
 }
 
-bool make_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16) {
-    const MapKey k{1, ptr, tiles, 0, 0, bf16};
+bool make_ds_map(CUtensorMap* m, const void* ptr, long long tiles, bool bf16, int rows = 128) {
+    const MapKey k{rows == 128 ? 1 : 3, ptr, tiles, 0, 0, bf16};
     if (g_maps.get(k, m)) {
         g_map_hits.fetch_add(1, std::memory_order_relaxed);
         return true;
     }
     g_map_misses.fetch_add(1, std::memory_order_relaxed);
-    if (!encode_ds_map(m, ptr, tiles, bf16)) return false;
+    if (!encode_ds_map(m, ptr, tiles, bf16, rows)) return false;
     g_maps.put(k, *m);
     return true;
 }
@@ -621,7 +622,7 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     p.dq_workers = W;
     p.dkdv_ctas = L.n_q * BH;
     p.n_units = BH;
-    p.ds_signals = DkdvCfg<kD>::kWG * L.n_q;
+    p.ds_signals = (kDsWarpStore<kD> ? 4 : 1) * DkdvCfg<kD>::kWG * L.n_q;
     p.dkdv_items = L.n_q * BH;
     // Persistent dK/dV (one CTA per SM looping over the (unit, key tile) items, static
     // round robin; the next item's K / V / Q / dO loads and first S / dP MMAs overlap the
@@ -654,6 +655,12 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
     CUtensorMap mds;
     if (L.materialize_ds && !make_ds_map(&mds, p.ds_out, static_cast<long long>(BH) * L.ds_tiles_per_bh, kBF16))
         return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled (dS) failed");
+    // per-warp dS^T stores (kDsWarpStore): 32-key boxes, passed in the non-pair kernel's
+    // (otherwise unused) 64-row Q map slot
+    CUtensorMap mds32 = mq;
+    if (kDsWarpStore<kD> && L.materialize_ds &&
+        !make_ds_map(&mds32, p.ds_out, static_cast<long long>(BH) * L.ds_tiles_per_bh, kBF16, 32))
+        return fail(VATTN_ECUDA, "cuTensorMapEncodeTiled (dS, 32-key boxes) failed");
     // 2) dK, dV (key-major)
     bool dkdv_launched = false;
     if constexpr (kD == 128) {
@@ -682,10 +689,10 @@ int launch_backward(const vattn_config* c, const void* q, const void* k, const v
         ProfScope prof(stream, 1);
         if (multi)
             launch_pdl(mha_bwd_dkdv_kernel<kD, kBF16, kDrop, false, true>, dim3(dkdv_ctas + W), dim3(DkdvCfg<kD>::kThreads),
-                       smem, stream, mq, mk, mv, mdo, L.materialize_ds ? mds : mq, mq, mdo, mdq, dk, dv, p);
+                       smem, stream, mq, mk, mv, mdo, L.materialize_ds ? mds : mq, mds32, mdo, mdq, dk, dv, p);
         else
             launch_pdl(mha_bwd_dkdv_kernel<kD, kBF16, kDrop, false, false>, dim3(dkdv_ctas + W), dim3(DkdvCfg<kD>::kThreads),
-                       smem, stream, mq, mk, mv, mdo, L.materialize_ds ? mds : mq, mq, mdo, mdq, dk, dv, p);
+                       smem, stream, mq, mk, mv, mdo, L.materialize_ds ? mds : mq, mds32, mdo, mdq, dk, dv, p);
     }
     // 3) dQ (query-major, fixed-order accumulation in TMEM)
     // The dQ GEMM runs as the persistent worker kernel (one CTA per SM looping over the

@@ -407,6 +407,15 @@ __global__ void __launch_bounds__(256, 1)
 #define VATTN_DKDV128_WG 2
 #endif
 template <int kD>
+struct DkdvCfg;
+// dS^T materialisation per warp (VATTN_DS_WARP_STORE, default on): each math warp stages
+// its 32 key rows and issues their TMA store itself, so the staging needs only __syncwarp
+// instead of two named barriers over the warpgroup per step.  Needs one warpgroup per
+// 64-query box (kQW = 64).
+#ifndef VATTN_DS_WARP_STORE
+#define VATTN_DS_WARP_STORE 1
+#endif
+template <int kD>
 struct DkdvCfg {
     static constexpr bool kDoubleS = kD == 64;
     static constexpr int kWG = kD == 64 ? VATTN_DKDV64_WG : VATTN_DKDV128_WG;  // math warpgroups
@@ -442,6 +451,8 @@ struct DkdvCfg {
     static constexpr uint32_t kTmemDP = kDoubleS ? 256 : 128;
     static constexpr uint32_t kTmemDV = kTmemDP + 128, kTmemDK = kTmemDV + kD;
 };
+template <int kD>
+constexpr bool kDsWarpStore = VATTN_DS_WARP_STORE != 0 && DkdvCfg<kD>::kQW == 64;
 
 // kPair (d = 128): a (2,1,1) cluster = two adjacent key tiles of one unit sharing
 // every query tile.  All four GEMMs run as cta_group::2 M = 256 MMAs issued by the
@@ -1005,6 +1016,22 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                 const bool ds_store_thread = (h % kBoxWG) == 0 && (warp & 3) == 0 && lane == 0;
                 const uint32_t bar_id = kBoxWG == 1 ? 1 + h : 5 + bx, bar_n = 128 * kBoxWG;
                 uint8_t* box = smem + Cfg::kSmemDsStage + bx * 16384;
+                if constexpr (kDsWarpStore<kD> && !kPair) {
+                    // this warp's 32 rows = a 4 KiB, 1 KiB-aligned slice of the box (the
+                    // 128-byte swizzle repeats every 8 rows): stage, fence, store it alone
+                    if (lane == 0) bulk_wait_read0();  // this warp's previous slice left
+                    __syncwarp();
+#pragma unroll
+                    for (int m = 0; m < kQW / 8; ++m)
+                        st_swz128(box, r, m, make_uint4(dsp[4 * m], dsp[4 * m + 1], dsp[4 * m + 2], dsp[4 * m + 3]));
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_3d(&tm_q64, box + (warp & 3) * 4096, 64 * bx, 32 * (warp & 3),
+                                     static_cast<int>(static_cast<long long>(bh) * p.ds_tiles_per_bh + ds_tile_index(p, i, kb)));
+                        bulk_commit();
+                    }
+                } else {
                 if (ds_store_thread) bulk_wait_read0();  // the previous box left the buffer
                 named_bar_sync(bar_id, bar_n);
                 const int m0 = (h % kBoxWG) * (kQW / 8);    // first 16-byte chunk of this warpgroup's row part
@@ -1018,11 +1045,12 @@ __global__ void __launch_bounds__(DkdvCfg<kD>::kThreads, 1)
                                  static_cast<int>(static_cast<long long>(bh) * p.ds_tiles_per_bh + ds_tile_index(p, i, kb)));
                     bulk_commit();
                 }
+                }
             }
 
             if ((warp == 4 || warp == 8) && lane == 0) VTRACE(1024 + 8 * s + 3 + (warp == 8 ? 4 : 0));
         }
-        if (p.ds_out && (warp & 3) == 0 && lane == 0) {
+        if (p.ds_out && ((kDsWarpStore<kD> && !kPair) || (warp & 3) == 0) && lane == 0) {
             if (p.dq_sync) {  // this CTA's dS^T stores are in memory: count them for the dQ workers
                 bulk_wait0();
                 fence_proxy_async_global();
