@@ -239,7 +239,7 @@ VATTN_DEV void dq_worker(const CUtensorMap* tm_ds, const CUtensorMap* tm_k, cons
     uint64_t* empty = bars + S;
     uint64_t* dq_done = bars + 2 * S;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
-    volatile int* s_item = reinterpret_cast<volatile int*>(tmem_slot + 1);
+    volatile int* s_item = reinterpret_cast<volatile int*>(tmem_slot + 1);  // [2]
     const int warp = warp_id();
     const int lane = lane_id();
     if (threadIdx.x == 0) {
@@ -264,45 +264,65 @@ VATTN_DEV void dq_worker(const CUtensorMap* tm_ds, const CUtensorMap* tm_k, cons
         tma_prefetch_desc(tm_k);
         tma_prefetch_desc(tm_dq);
     }
-    for (;;) {
-        if (threadIdx.x == 0) {
-            int item = -1;
-            if (!early || ld_acquire_gpu(p.dq_sync + 1) < p.dkdv_ctas) {
-                item = atomicAdd(p.dq_sync, 1);
-                if (item >= total) {
-                    item = -1;
-                } else if (early) {
-                    const int* cnt = p.dq_sync + 2 + item / nq;
-                    const uint64_t t0 = globaltimer_ns();
-                    while (ld_acquire_gpu(cnt) < p.ds_signals) {
-                        __nanosleep(500);
-                        if (VATTN_WATCHDOG_NS && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) __trap();
-                    }
-                    fence_proxy_async_global();  // the TMA loads below see the dS^T stores
+    // Items come from the atomic counter (thread 0 = the producer lane).  The producer
+    // takes the NEXT item as soon as it has issued the current one's loads and prefetches
+    // its first min(S, tiles) dS^T / K tiles into the ring stages this item's MMAs free,
+    // so those loads run under this item's epilogue instead of after the CTA barrier
+    // (s_item: two slots, the next item's published before the end-of-item barrier).
+    auto fetch = [&]() -> int {
+        int item = -1;
+        if (!early || ld_acquire_gpu(p.dq_sync + 1) < p.dkdv_ctas) {
+            item = atomicAdd(p.dq_sync, 1);
+            if (item >= total) {
+                item = -1;
+            } else if (early) {
+                const int* cnt = p.dq_sync + 2 + item / nq;
+                const uint64_t t0 = globaltimer_ns();
+                while (ld_acquire_gpu(cnt) < p.ds_signals) {
+                    __nanosleep(500);
+                    if (VATTN_WATCHDOG_NS && globaltimer_ns() - t0 > VATTN_WATCHDOG_NS) __trap();
                 }
+                fence_proxy_async_global();  // the TMA loads below see the dS^T stores
             }
-            *s_item = item;
         }
-        __syncthreads();
-        const int item = *s_item;
+        return item;
+    };
+    auto decode = [&](int item, int& bh, int& i, int& nk) {
+        bh = item / nq;
+        const int tile = item - bh * nq;
+        i = p.causal ? (nq - 1 - tile) : tile;
+        nk = p.causal ? i + 1 : nq;
+    };
+    auto issue = [&](int bh, int i, uint32_t q, int j) {  // dS^T tile (i, j) and K_j into ring slot q
+        const int st = q % S;
+        mbar_wait<VATTN_SLEEP_PRODUCER>(empty + st, ((q / S) & 1) ^ 1);
+        mbar_arrive_expect_tx(full + st, Cfg::kStageBytes);
+        uint8_t* ds = smem + st * Cfg::kStageBytes;
+        uint8_t* kt = ds + Cfg::kDsBytes;
+        const int tl = static_cast<int>(static_cast<long long>(bh) * p.ds_tiles_per_bh + ds_tile_index(p, i, j));
+        tma_load_3d(ds, tm_ds, full + st, 0, 0, tl);
+        tma_load_3d(ds + 16384, tm_ds, full + st, 64, 0, tl);
+        for (int b = 0; b < kD / 64; ++b) tma_load_3d(kt + b * 16384, tm_k, full + st, b * 64, j * 128, bh);
+    };
+    if (threadIdx.x == 0) s_item[0] = fetch();
+    __syncthreads();
+    int pre = 0;  // producer: tiles of the current item issued during the previous one
+    for (;;) {
+        const int item = s_item[it & 1];
         if (item < 0) break;
-        const int bh = item / nq, tile = item - bh * nq;
-        const int i = p.causal ? (nq - 1 - tile) : tile;
-        const int nk = p.causal ? i + 1 : nq;
+        int bh, i, nk;
+        decode(item, bh, i, nk);
         if (warp == 0) {
             if (lane == 0) {
-                const long long tile0 = static_cast<long long>(bh) * p.ds_tiles_per_bh + ds_tile_index(p, i, 0);
-                for (int j = 0; j < nk; ++j) {
-                    const uint32_t q = pos + j;
-                    const int st = q % S;
-                    mbar_wait<VATTN_SLEEP_PRODUCER>(empty + st, ((q / S) & 1) ^ 1);
-                    mbar_arrive_expect_tx(full + st, Cfg::kStageBytes);
-                    uint8_t* ds = smem + st * Cfg::kStageBytes;
-                    uint8_t* kt = ds + Cfg::kDsBytes;
-                    const int tl = static_cast<int>(tile0 + j);
-                    tma_load_3d(ds, tm_ds, full + st, 0, 0, tl);
-                    tma_load_3d(ds + 16384, tm_ds, full + st, 64, 0, tl);
-                    for (int b = 0; b < kD / 64; ++b) tma_load_3d(kt + b * 16384, tm_k, full + st, b * 64, j * 128, bh);
+                for (int j = pre; j < nk; ++j) issue(bh, i, pos + j, j);
+                const int nxt = fetch();
+                s_item[(it + 1) & 1] = nxt;
+                pre = 0;
+                if (nxt >= 0) {
+                    int bh2, i2, nk2;
+                    decode(nxt, bh2, i2, nk2);
+                    pre = nk2 < S ? nk2 : S;
+                    for (int j = 0; j < pre; ++j) issue(bh2, i2, pos + nk + j, j);
                 }
             }
         } else if (warp == 1) {
